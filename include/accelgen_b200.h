@@ -1,0 +1,155 @@
+/*
+ * accelgen_b200.h -- C ABI of the B200 mixed-batch forward (libaccelgen_b200.so).
+ *
+ * This library replaces ONE call in the reference: the simulated GPU step.  In the reference,
+ * engine.step "advance[s] clock by iteration_time(S_f)" where iteration_time is
+ * the linear stand-in  T_0 + T_pf * S_f / S_pf  (pkg/src/slosim/cost_model.py:133-141).  Here the
+ * BatchPlan that AccelGen's policy packs is executed on the GPU instead:
+ * embedding -> L x [LN, QKV(+paged KV append), mixed paged attention, out-proj(+TP all-reduce),
+ * LN, FC1+ReLU, FC2(+TP all-reduce)] -> final LN on the logit rows -> LM head -> argmax.
+ *
+ * Conventions
+ *   - Plain C types only; every device buffer is a raw pointer, every stream is a cudaStream_t
+ *     passed as void*.  bf16 tensors are uint16-storage bfloat16, row-major.
+ *   - Every function returns AG_OK (0) or an AG_E* code; ag_last_error() returns the message
+ *     (thread-local).  The Python host maps AG_EINVAL -> ValidationError, AG_EALLOC ->
+ *     AllocationError and AG_ECUDA / AG_EFAULT -> EngineFault (pkg/src/slosim/errors.py:16-32).
+ *   - KV pool layout per layer and per K/V: [num_blocks][heads_local][block_size=32][head_dim=128]
+ *     bf16; block ids are the physical ids assigned by the scheduler's BlockPool
+ *     (the reference tracks counts only, pkg/src/slosim/kvc.py:42-45).
+ */
+#ifndef ACCELGEN_B200_H_
+#define ACCELGEN_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define AG_API __attribute__((visibility("default")))
+#else
+#define AG_API
+#endif
+
+#define AG_OK 0
+#define AG_EINVAL 1  /* bad argument / shape */
+#define AG_ECUDA 2   /* CUDA runtime or launch error */
+#define AG_EALLOC 3  /* capacity exceeded (tokens, sequences, workspace) */
+#define AG_EFAULT 4  /* internal invariant violation (reference: EngineFault, errors.py:28-32) */
+#define AG_ENCCL 5   /* NCCL error (tensor parallel) */
+
+typedef struct ag_model ag_model; /* opaque */
+
+/* Model shape and capacities.  Mirrors the reference ModelProfile's shape fields
+ * (cost_model.py:66-76: hidden_size, num_layers, bytes_per_element) plus the OPT architecture
+ * constants the cost model folds away. */
+typedef struct {
+  int32_t hidden;          /* H (5120 for OPT-13B) */
+  int32_t num_layers;      /* L */
+  int32_t num_heads;       /* total heads; head_dim = hidden / num_heads must be 128 */
+  int32_t ffn;             /* FC1 width (4H) */
+  int32_t vocab;           /* V (50272) */
+  int32_t pos_rows;        /* rows of the learned position table (incl. OPT offset 2) */
+  int32_t tp_rank;
+  int32_t tp_size;         /* 1, 2, 4, 8: heads, ffn and vocab must divide */
+  int32_t num_blocks;      /* KV pool blocks (kvc_capacity_tokens // 32, kvc.py:47-50) */
+  int32_t block_size;      /* 32 (kvc.py:16) */
+  int32_t max_tokens;      /* max forward size S_f per step */
+  int32_t max_seqs;        /* max sequences per step */
+  int32_t max_blocks_per_seq; /* block-table row stride */
+  float ln_eps;            /* 1e-5 */
+} ag_model_config;
+
+/* Per-layer weights (device pointers, bf16, nn.Linear layout [out, in]); this rank's shard. */
+typedef struct {
+  const void* ln1_g; const void* ln1_b;     /* [H] */
+  const void* qkv_w; const void* qkv_b;     /* [3*Hl, H], [3*Hl]   (q | k | v, Hl = H/tp) */
+  const void* out_w; const void* out_b;     /* [H, Hl], [H] */
+  const void* ln2_g; const void* ln2_b;     /* [H] */
+  const void* fc1_w; const void* fc1_b;     /* [F/tp, H], [F/tp] */
+  const void* fc2_w; const void* fc2_b;     /* [H, F/tp], [H] */
+} ag_layer_weights;
+
+/* One iteration's packed BatchPlan (HOST pointers).  B sequences; sequence b contributes
+ * q_b = cu_q[b+1]-cu_q[b] new tokens (a prompt chunk, or one decode token)
+ * on top of ctx_len[b] tokens already in its KV blocks. */
+typedef struct {
+  int32_t num_tokens;           /* S_f = sum of chunk lengths */
+  int32_t num_seqs;             /* B */
+  int32_t num_logits;           /* rows that emit a token (final chunks + TG steps) */
+  int32_t block_table_stride;   /* >= max blocks of any sequence, <= max_blocks_per_seq */
+  const int32_t* token_ids;     /* [S_f] */
+  const int32_t* positions;     /* [S_f] absolute positions (0-based) */
+  const int32_t* cu_q;          /* [B+1] */
+  const int32_t* ctx_len;       /* [B] */
+  const int32_t* block_table;   /* [B, stride] physical block ids */
+  const int32_t* slot_mapping;  /* [S_f] block*32+offset of each new token's KV slot */
+  const int32_t* logit_rows;    /* [num_logits] token rows whose logits are needed */
+} ag_step;
+
+AG_API const char* ag_last_error(void);
+AG_API int32_t ag_version(void);
+AG_API int32_t ag_device_sm_count(void);
+
+/* ---- model lifecycle (reference boundary: engine.step's clock advance) ---- */
+AG_API int32_t ag_model_create(const ag_model_config* cfg, ag_model** out);
+AG_API void ag_model_destroy(ag_model* m);
+AG_API int32_t ag_model_set_embeddings(ag_model* m, const void* tok_emb /*[V,H]*/, const void* pos_emb /*[pos_rows,H]*/,
+                                const void* final_ln_g, const void* final_ln_b);
+AG_API int32_t ag_model_set_layer(ag_model* m, int32_t layer, const ag_layer_weights* w);
+AG_API int32_t ag_model_set_kv_cache(ag_model* m, int32_t layer, void* k_pool, void* v_pool);
+/* Tensor parallel: rank 0 calls ag_nccl_get_unique_id, the 128 bytes are broadcast by the host,
+ * then every rank calls ag_model_init_tp (NCCL communicator over NVLink, in-stream all-reduce). */
+AG_API int32_t ag_nccl_get_unique_id(void* out_128_bytes);
+AG_API int32_t ag_model_init_tp(ag_model* m, const void* unique_id_128_bytes);
+
+/* Execute one BatchPlan.  Host metadata is packed into one pinned buffer, copied H2D on
+ * `stream`, the forward runs, and next-token ids are copied back into out_tokens (host, int32
+ * [num_logits]).  If logits_out (device, f32 [num_logits, vocab/tp]) is non-null the local logit
+ * shard is also written (parity mode).  device_ms (optional) receives the CUDA-event time of the
+ * forward alone (metadata already resident, before the D2H).  Synchronises `stream`. */
+AG_API int32_t ag_model_forward(ag_model* m, const ag_step* step, int32_t* out_tokens, float* logits_out,
+                         float* device_ms, void* stream);
+
+/* Same forward, asynchronous, with all metadata already packed in device memory by
+ * ag_model_stage_step (used to time the kernels with inputs resident in HBM). */
+AG_API int32_t ag_model_stage_step(ag_model* m, const ag_step* step, void* stream);
+AG_API int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* logits_out, void* stream);
+
+/* ---- individual kernels (device pointers), for parity tests and the profiler ---- */
+/* D[M,N] = A[M,K] . W[N,K]^T (+bias[N]) (+residual[M,ldr]) (ReLU); bf16 out unless out_f32. */
+AG_API int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias,
+                     const void* residual, int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32,
+                     int32_t M, int32_t N, int32_t K, int32_t block_n, void* stream);
+/* Paged KV append: rows of k/v ([rows, heads*128], row stride ld) into their slots. */
+AG_API int32_t ag_kv_append(const void* k, const void* v, int32_t ld, const int32_t* slot_mapping, int32_t rows,
+                     int32_t heads, int32_t block_size, void* k_pool, void* v_pool, void* stream);
+/* Mixed paged attention over B sequences (q already scaled by head_dim^-0.5).  cu_q/ctx_len are
+ * given on both host (work-list construction) and device. */
+AG_API int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const void* v_pool,
+                           const int32_t* block_table_dev, int32_t bt_stride, const int32_t* cu_q_host,
+                           const int32_t* ctx_len_host, const int32_t* cu_q_dev, const int32_t* ctx_len_dev,
+                           int32_t num_seqs, int32_t heads, int32_t block_size, void* out, int32_t ldo,
+                           void* workspace, int64_t workspace_bytes, void* stream);
+AG_API int32_t ag_layernorm(void* x, const void* delta, const void* delta_bias, const int32_t* row_index,
+                     const void* gamma, const void* beta, float eps, int32_t rows, int32_t hidden, void* out,
+                     void* stream);
+AG_API int32_t ag_embed_pos(const int32_t* ids, const int32_t* positions, const void* tok_emb, const void* pos_emb,
+                     int32_t pos_offset, int32_t rows, int32_t hidden, int32_t vocab, int32_t pos_rows,
+                     void* out, void* stream);
+AG_API int32_t ag_argmax(const float* logits, int32_t rows, int32_t cols, int32_t ld, int32_t index_offset,
+                  float* out_val, int32_t* out_idx, void* stream);
+/* Preemption swap (reference BlockPool.preempt / demand_readmit, kvc.py:110-116,153-160):
+ * gather blocks of one pool into a contiguous buffer (swap out) or scatter them back (swap in). */
+AG_API int32_t ag_kv_swap_out(const void* pool, const int32_t* block_ids_dev, int32_t n_blocks, int64_t block_elems,
+                       void* staging, void* stream);
+AG_API int32_t ag_kv_swap_in(const void* staging, const int32_t* block_ids_dev, int32_t n_blocks, int64_t block_elems,
+                      void* pool, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACCELGEN_B200_H_ */

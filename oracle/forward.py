@@ -1,0 +1,155 @@
+"""CPU ORACLE of the mixed-batch OPT forward — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+import this module.  The product path (paper_2503_13737_b200) never does.
+
+What it restates
+  The reference ships no forward pass: its "GPU" is the linear stand-in iteration_time
+  (pkg/src/slosim/cost_model.py:133-141) and the paper's executor was vLLM + FlashAttention-2
+  (PAPER.md:2002-2009), neither of which is under /root/reference.  Logit parity is therefore
+  "parity unpinned" by the reference itself.  This oracle restates the OPT decoder the paper
+  serves (per-layer QKV, attention, out-proj, FC1, FC2, residuals; the operation
+  counts of Eq. 1-4 at PAPER.md:491-498) with the OPT details of transformers 5.5.0
+  modeling_opt.py (learned positions offset 2, q*head_dim^-0.5, pre-LN, ReLU, tied LM head),
+  executed over a PAGED KV cache driven by the same BatchPlan metadata as the GPU.  It is pinned
+  against transformers' OPTForCausalLM by tests/golden/opt_tiny_hf.pt (tests/golden/make_golden.py).
+
+Rounding points mirror the device kernels: activations are stored in bf16 between kernels
+(q after scaling, K/V in the cache, attention output, residual stream, LN outputs, FC1 output);
+every matmul accumulates in fp32; softmax and LN statistics are fp32; logits stay fp32.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+POS_OFFSET = 2
+HEAD_DIM = 128
+
+
+def rb(x: torch.Tensor) -> torch.Tensor:
+    """Round to bf16 and return as fp32 (a storage point of the device pipeline)."""
+    return x.to(torch.bfloat16).to(torch.float32)
+
+
+def f32(x: torch.Tensor) -> torch.Tensor:
+    return x.detach().to("cpu", torch.float32)
+
+
+def embed(ids, positions, tok_emb, pos_emb):
+    return rb(f32(tok_emb)[ids.long()] + f32(pos_emb)[positions.long() + POS_OFFSET])
+
+
+def layernorm(x, g, b, eps=1e-5):
+    mean = x.mean(-1, keepdim=True)
+    var = ((x - mean) ** 2).mean(-1, keepdim=True)
+    return rb((x - mean) * torch.rsqrt(var + eps) * f32(g) + f32(b))
+
+
+def paged_attention(q, k_pool, v_pool, block_table, cu_q, ctx_len, block_size=32):
+    """q [S, heads*128] (already scaled); pools [blocks, heads, bs, 128]; returns fp32 [S, heads*128].
+
+    Sequence b's query row i sits at position ctx_len[b] + i and attends to kv positions
+    0..ctx_len[b]+i of the sequence's pages (causal, prefix cache included)."""
+    S = q.shape[0]
+    heads = k_pool.shape[1]
+    out = torch.zeros(S, heads * HEAD_DIM, dtype=torch.float32)
+    cu_q = [int(v) for v in cu_q]
+    for b in range(len(cu_q) - 1):
+        q0, q1 = cu_q[b], cu_q[b + 1]
+        if q1 == q0:
+            continue
+        n_q = q1 - q0
+        ctx = int(ctx_len[b])
+        kv_len = ctx + n_q
+        n_pages = (kv_len + block_size - 1) // block_size
+        pages = block_table[b, :n_pages].long()
+        k = f32(k_pool[pages]).permute(1, 0, 2, 3).reshape(heads, n_pages * block_size, HEAD_DIM)[:, :kv_len]
+        v = f32(v_pool[pages]).permute(1, 0, 2, 3).reshape(heads, n_pages * block_size, HEAD_DIM)[:, :kv_len]
+        qb = q[q0:q1].reshape(n_q, heads, HEAD_DIM).permute(1, 0, 2)
+        s = qb @ k.transpose(1, 2)  # [heads, n_q, kv_len]
+        qpos = ctx + torch.arange(n_q).unsqueeze(1)
+        kpos = torch.arange(kv_len).unsqueeze(0)
+        s = s.masked_fill(kpos > qpos, float("-inf"))
+        p = torch.softmax(s, dim=-1)
+        o = p @ v  # [heads, n_q, 128]
+        out[q0:q1] = o.permute(1, 0, 2).reshape(n_q, heads * HEAD_DIM)
+    return out
+
+
+def kv_append(k_rows, v_rows, slot_mapping, k_pool, v_pool, block_size=32):
+    """Write rows [S, heads*128] into their (block, offset) slots; slots < 0 are skipped."""
+    heads = k_pool.shape[1]
+    for i, slot in enumerate(slot_mapping.tolist()):
+        if slot < 0:
+            continue
+        blk, off = divmod(slot, block_size)
+        k_pool[blk, :, off, :] = k_rows[i].reshape(heads, HEAD_DIM).to(k_pool.dtype)
+        v_pool[blk, :, off, :] = v_rows[i].reshape(heads, HEAD_DIM).to(v_pool.dtype)
+
+
+@dataclass
+class StepInputs:
+    """The packed BatchPlan of one iteration (same fields as the C-ABI ag_step)."""
+    token_ids: torch.Tensor
+    positions: torch.Tensor
+    cu_q: torch.Tensor
+    ctx_len: torch.Tensor
+    block_table: torch.Tensor
+    slot_mapping: torch.Tensor
+    logit_rows: torch.Tensor
+
+
+class OracleOPT:
+    """Paged-KV OPT forward on the CPU.  ``weights`` follows paper_2503_13737_b200.model.init_weights
+    (full model, tp_size=1) or one TP shard when tp_size > 1 (then ``allreduce`` sums partials)."""
+
+    def __init__(self, cfg, weights, num_blocks, block_size=32, tp_rank=0, tp_size=1, allreduce=None):
+        self.cfg = cfg
+        self.w = weights
+        self.block_size = block_size
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.allreduce = allreduce
+        heads_l = cfg.num_heads // tp_size
+        self.heads_l = heads_l
+        self.k_pools = [torch.zeros(num_blocks, heads_l, block_size, HEAD_DIM, dtype=torch.bfloat16)
+                        for _ in range(cfg.num_layers)]
+        self.v_pools = [torch.zeros_like(p) for p in self.k_pools]
+        self.scale = 1.0 / math.sqrt(HEAD_DIM)
+
+    def _reduce(self, partial):
+        if self.tp_size == 1:
+            return partial
+        return self.allreduce(partial)
+
+    def forward(self, st: StepInputs):
+        cfg, w = self.cfg, self.w
+        hq = self.heads_l * HEAD_DIM
+        x = embed(st.token_ids, st.positions, w["tok_emb"], w["pos_emb"])
+        for l, L in enumerate(w["layers"]):
+            h = layernorm(x, L["ln1_g"], L["ln1_b"], cfg.ln_eps)
+            qkv = h @ f32(L["qkv_w"]).T + f32(L["qkv_b"])
+            q = rb(qkv[:, :hq] * self.scale)
+            k = rb(qkv[:, hq:2 * hq])
+            v = rb(qkv[:, 2 * hq:])
+            kv_append(k, v, st.slot_mapping, self.k_pools[l], self.v_pools[l], self.block_size)
+            a = rb(paged_attention(q, self.k_pools[l], self.v_pools[l], st.block_table, st.cu_q, st.ctx_len,
+                                   self.block_size))
+            if self.tp_size == 1:
+                x = rb(a @ f32(L["out_w"]).T + f32(L["out_b"]) + x)
+            else:
+                part = self._reduce(rb(a @ f32(L["out_w"]).T))
+                x = rb(x + (part + f32(L["out_b"])))
+            h = layernorm(x, L["ln2_g"], L["ln2_b"], cfg.ln_eps)
+            f = rb(torch.relu(h @ f32(L["fc1_w"]).T + f32(L["fc1_b"])))
+            if self.tp_size == 1:
+                x = rb(f @ f32(L["fc2_w"]).T + f32(L["fc2_b"]) + x)
+            else:
+                part = self._reduce(rb(f @ f32(L["fc2_w"]).T))
+                x = rb(x + (part + f32(L["fc2_b"])))
+        rows = st.logit_rows.long()
+        hl = layernorm(x[rows], w["final_g"], w["final_b"], cfg.ln_eps)
+        logits = hl @ f32(w["tok_emb"]).T
+        return logits, torch.argmax(logits, dim=-1).to(torch.int32)

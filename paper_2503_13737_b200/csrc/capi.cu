@@ -1,0 +1,721 @@
+// C-ABI layer: model object, BatchPlan packing, the per-layer launch sequence and the
+// standalone kernel entry points declared in include/accelgen_b200.h.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/accelgen_b200.h"
+#include "kernels.h"
+
+using ag::AttnCombine;
+using ag::AttnItem;
+using bf16 = __nv_bfloat16;
+
+namespace {
+
+thread_local std::string g_err;
+
+int32_t fail(int32_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define AG_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(AG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+#define AG_TRY(expr)                    \
+  do {                                  \
+    int32_t _r = (expr);                \
+    if (_r != AG_OK) return _r;         \
+  } while (0)
+
+// ---------------------------------------------------------------- NCCL (dlopen'd)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather &&
+               api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+// ---------------------------------------------------------------- attention work list
+struct AttnWork {
+  std::vector<AttnItem> items;
+  std::vector<AttnCombine> combines;
+  int part_rows = 0;
+};
+
+// Tile every sequence's new tokens into <=64-row query tiles (<=16 rows run in decode mode) and
+// split long KV ranges so that ~4 CTAs per SM of work exist; splits are multiples of 64 tokens.
+void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, int heads, int part_cap,
+                          AttnWork& w) {
+  w.items.clear();
+  w.combines.clear();
+  w.part_rows = 0;
+  struct Tile {
+    int seq, qs, rows, kv_hi;
+    double cost;
+  };
+  std::vector<Tile> tiles;
+  double total = 0.0;
+  for (int b = 0; b < B; ++b) {
+    const int q = cu_q[b + 1] - cu_q[b];
+    if (q <= 0) continue;
+    const int T = q <= 16 ? 16 : 64;
+    for (int qs = 0; qs < q; qs += T) {
+      const int rows = std::min(T, q - qs);
+      const int kv_hi = ctx_len[b] + qs + rows;
+      const double c = static_cast<double>(kv_hi) * (rows > 16 ? 4.0 : 1.0);
+      tiles.push_back({b, qs, rows, kv_hi, c});
+      total += c;
+    }
+  }
+  const int desired = std::max(1, (ag::num_sms() * 4 + heads - 1) / heads);
+  const double per_item = std::max(1.0, total / desired);
+  for (const Tile& t : tiles) {
+    int n_split = static_cast<int>(std::ceil(t.cost / per_item));
+    n_split = std::max(1, std::min(n_split, (t.kv_hi + 255) / 256));
+    int split = (t.kv_hi + n_split - 1) / n_split;
+    split = (split + 63) / 64 * 64;
+    n_split = (t.kv_hi + split - 1) / split;
+    if (n_split > 1 && w.part_rows + n_split * t.rows > part_cap) n_split = 1;
+    if (n_split == 1) {
+      w.items.push_back({t.seq, t.qs, t.rows, 0, t.kv_hi, -1, 0, 0});
+      continue;
+    }
+    const int base = w.part_rows;
+    for (int s = 0; s < n_split; ++s) {
+      const int a = s * split;
+      const int e = std::min(t.kv_hi, a + split);
+      w.items.push_back({t.seq, t.qs, t.rows, a, e, base + s * t.rows, 0, 0});
+    }
+    w.combines.push_back({cu_q[t.seq] + t.qs, t.rows, base, n_split});
+    w.part_rows += n_split * t.rows;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- model object
+// A weight operand needs one tensor map per N-tile width (the TMA box must equal BLOCK_N).
+struct WeightMap {
+  CUtensorMap box128, box256;
+  bool has256 = false;
+};
+
+struct LayerState {
+  ag_layer_weights w{};
+  bf16* kpool = nullptr;
+  bf16* vpool = nullptr;
+  WeightMap tm_qkv, tm_out, tm_fc1, tm_fc2;
+  bool ready = false;
+};
+
+struct ag_model {
+  ag_model_config cfg{};
+  int head_dim = 128, heads_l = 0, hq = 0, ffn_l = 0, vocab_l = 0, vocab_off = 0;
+  std::vector<LayerState> layers;
+  const bf16* tok_emb = nullptr;
+  const bf16* pos_emb = nullptr;
+  const bf16* final_g = nullptr;
+  const bf16* final_b = nullptr;
+  // activations
+  bf16 *resid = nullptr, *xln = nullptr, *qbuf = nullptr, *attn = nullptr, *ffn = nullptr, *proj = nullptr;
+  bf16* lm_in = nullptr;
+  float* logits = nullptr;
+  float* cand_val = nullptr;
+  int32_t* cand_idx = nullptr;
+  float* gathered_val = nullptr;
+  int32_t* gathered_idx = nullptr;
+  int32_t* out_tok = nullptr;
+  float *part_o = nullptr, *part_ml = nullptr;
+  int part_cap = 0;
+  // metadata: one pinned host buffer mirrored by one device buffer
+  uint8_t* meta_host = nullptr;
+  uint8_t* meta_dev = nullptr;
+  size_t meta_cap = 0;
+  int32_t* tok_host = nullptr;  // pinned D2H staging
+  CUtensorMap tm_xln, tm_attn, tm_ffn, tm_lm_in;
+  WeightMap tm_lm_w;
+  // staged step
+  int S = 0, B = 0, n_logit = 0, bt_stride = 0, n_items = 0, n_comb = 0;
+  const int32_t *d_ids = nullptr, *d_pos = nullptr, *d_cuq = nullptr, *d_ctx = nullptr, *d_bt = nullptr,
+                *d_slot = nullptr, *d_lrows = nullptr;
+  const AttnItem* d_items = nullptr;
+  const AttnCombine* d_comb = nullptr;
+  AttnWork work;
+  ncclComm_t comm = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int32_t dmalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) return fail(AG_EALLOC, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return AG_OK;
+}
+
+int32_t tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t k, int box_rows, const char* what) {
+  const int r = ag::make_tmap_kmajor(m, ptr, rows, k, k, box_rows);
+  if (r != 0) return fail(AG_EINVAL, std::string("tensor map for ") + what + " failed (" + std::to_string(r) + ")");
+  return AG_OK;
+}
+
+int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char* what) {
+  AG_TRY(tmap(&w->box128, ptr, rows, k, 128, what));
+  w->has256 = rows % 256 == 0;
+  if (w->has256) AG_TRY(tmap(&w->box256, ptr, rows, k, 256, what));
+  return AG_OK;
+}
+
+// GEMM against a weight: choose the N tile, then the matching tensor map.
+cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
+                   cudaStream_t s) {
+  int bn = ag::pick_block_n(M, N);
+  if (bn == 256 && !w.has256) bn = 128;
+  return ag::launch_gemm(a, bn == 256 ? w.box256 : w.box128, M, N, K, bn, ep, 0, s);
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int32_t check_nccl(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return AG_OK;
+  return fail(AG_ENCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+int32_t allreduce_bf16(ag_model* m, bf16* buf, size_t count, cudaStream_t s) {
+  if (m->cfg.tp_size == 1) return AG_OK;
+  return check_nccl(nccl().AllReduce(buf, buf, count, ncclBfloat16, ncclSum, m->comm, s), "ncclAllReduce");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ag_last_error(void) { return g_err.c_str(); }
+int32_t ag_version(void) { return 1; }
+int32_t ag_device_sm_count(void) { return ag::num_sms(); }
+
+int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
+  if (!cfg || !out) return fail(AG_EINVAL, "null argument");
+  const ag_model_config& c = *cfg;
+  if (c.hidden <= 0 || c.num_layers <= 0 || c.num_heads <= 0 || c.hidden % c.num_heads != 0)
+    return fail(AG_EINVAL, "bad hidden/num_heads");
+  if (c.hidden / c.num_heads != 128) return fail(AG_EINVAL, "head_dim must be 128");
+  if (c.tp_size < 1 || c.tp_rank < 0 || c.tp_rank >= c.tp_size) return fail(AG_EINVAL, "bad tp rank/size");
+  if (c.num_heads % c.tp_size || c.ffn % c.tp_size || c.vocab % c.tp_size)
+    return fail(AG_EINVAL, "heads, ffn and vocab must divide by tp_size");
+  if (c.block_size != 32) return fail(AG_EINVAL, "block_size must be 32");
+  if (c.max_tokens <= 0 || c.max_seqs <= 0 || c.max_blocks_per_seq <= 0 || c.num_blocks <= 0)
+    return fail(AG_EINVAL, "capacities must be positive");
+  if (c.hidden % 64 || (c.ffn / c.tp_size) % 64 || (c.vocab / c.tp_size) % 32)
+    return fail(AG_EINVAL, "hidden, ffn/tp must be multiples of 64 and vocab/tp of 32");
+
+  ag_model* m = new ag_model();
+  m->cfg = c;
+  m->heads_l = c.num_heads / c.tp_size;
+  m->hq = m->heads_l * m->head_dim;
+  m->ffn_l = c.ffn / c.tp_size;
+  m->vocab_l = c.vocab / c.tp_size;
+  m->vocab_off = c.tp_rank * m->vocab_l;
+  m->layers.resize(c.num_layers);
+  // activation rows are padded to a multiple of 128 so GEMM A-tiles never leave the buffer
+  const size_t T = align_up(static_cast<size_t>(c.max_tokens), 128);
+  const size_t Sq = align_up(static_cast<size_t>(c.max_seqs), 128);
+  int32_t r = AG_OK;
+  auto chk = [&](int32_t x) {
+    if (r == AG_OK) r = x;
+  };
+  chk(dmalloc(&m->resid, T * c.hidden));
+  chk(dmalloc(&m->xln, T * c.hidden));
+  chk(dmalloc(&m->qbuf, T * m->hq));
+  chk(dmalloc(&m->attn, T * m->hq));
+  chk(dmalloc(&m->ffn, T * m->ffn_l));
+  chk(dmalloc(&m->proj, T * c.hidden));
+  chk(dmalloc(&m->lm_in, Sq * c.hidden));
+  chk(dmalloc(&m->logits, Sq * m->vocab_l));
+  chk(dmalloc(&m->cand_val, Sq));
+  chk(dmalloc(&m->cand_idx, Sq));
+  chk(dmalloc(&m->gathered_val, Sq * c.tp_size));
+  chk(dmalloc(&m->gathered_idx, Sq * c.tp_size));
+  chk(dmalloc(&m->out_tok, Sq));
+  m->part_cap = std::max(4096, c.max_tokens * 4);
+  chk(dmalloc(&m->part_o, static_cast<size_t>(m->part_cap) * m->heads_l * m->head_dim));
+  chk(dmalloc(&m->part_ml, static_cast<size_t>(m->part_cap) * m->heads_l * 2));
+  // metadata capacity: token arrays, sequence arrays, block table, attention work list
+  const size_t max_items = static_cast<size_t>(c.max_tokens) + c.max_seqs + 64 * static_cast<size_t>(ag::num_sms());
+  m->meta_cap = align_up(4 * sizeof(int32_t) * T, 256) + align_up(2 * sizeof(int32_t) * (c.max_seqs + 1), 256) +
+                align_up(sizeof(int32_t) * static_cast<size_t>(c.max_seqs) * c.max_blocks_per_seq, 256) +
+                align_up(sizeof(AttnItem) * max_items, 256) + align_up(sizeof(AttnCombine) * max_items, 256) + 4096;
+  if (r == AG_OK && cudaMallocHost(&m->meta_host, m->meta_cap) != cudaSuccess) r = fail(AG_EALLOC, "pinned alloc");
+  chk(dmalloc(&m->meta_dev, m->meta_cap));
+  if (r == AG_OK && cudaMallocHost(&m->tok_host, Sq * sizeof(int32_t)) != cudaSuccess) r = fail(AG_EALLOC, "pinned");
+  if (r == AG_OK) {
+    chk(tmap(&m->tm_xln, m->xln, T, c.hidden, 128, "xln"));
+    chk(tmap(&m->tm_attn, m->attn, T, m->hq, 128, "attn"));
+    chk(tmap(&m->tm_ffn, m->ffn, T, m->ffn_l, 128, "ffn"));
+    chk(tmap(&m->tm_lm_in, m->lm_in, Sq, c.hidden, 128, "lm_in"));
+  }
+  if (r == AG_OK) {
+    cudaEventCreate(&m->ev0);
+    cudaEventCreate(&m->ev1);
+  }
+  if (r != AG_OK) {
+    std::string keep = g_err;
+    ag_model_destroy(m);
+    g_err = keep;
+    return r;
+  }
+  *out = m;
+  return AG_OK;
+}
+
+void ag_model_destroy(ag_model* m) {
+  if (!m) return;
+  if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
+  void* dev[] = {m->resid, m->xln, m->qbuf, m->attn, m->ffn, m->proj, m->lm_in, m->logits, m->cand_val,
+                 m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (m->meta_host) cudaFreeHost(m->meta_host);
+  if (m->tok_host) cudaFreeHost(m->tok_host);
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
+  delete m;
+}
+
+int32_t ag_model_set_embeddings(ag_model* m, const void* tok_emb, const void* pos_emb, const void* final_ln_g,
+                                const void* final_ln_b) {
+  if (!m || !tok_emb || !pos_emb || !final_ln_g || !final_ln_b) return fail(AG_EINVAL, "null argument");
+  m->tok_emb = static_cast<const bf16*>(tok_emb);
+  m->pos_emb = static_cast<const bf16*>(pos_emb);
+  m->final_g = static_cast<const bf16*>(final_ln_g);
+  m->final_b = static_cast<const bf16*>(final_ln_b);
+  // tied LM head: this rank's vocab shard of the token embedding
+  return wmap(&m->tm_lm_w, m->tok_emb + static_cast<size_t>(m->vocab_off) * m->cfg.hidden, m->vocab_l,
+              m->cfg.hidden, "lm head");
+}
+
+int32_t ag_model_set_layer(ag_model* m, int32_t layer, const ag_layer_weights* w) {
+  if (!m || !w || layer < 0 || layer >= m->cfg.num_layers) return fail(AG_EINVAL, "bad layer");
+  const void* req[] = {w->ln1_g, w->ln1_b, w->qkv_w, w->qkv_b, w->out_w, w->out_b,
+                       w->ln2_g, w->ln2_b, w->fc1_w, w->fc1_b, w->fc2_w, w->fc2_b};
+  for (const void* p : req)
+    if (!p) return fail(AG_EINVAL, "null weight pointer");
+  LayerState& L = m->layers[layer];
+  L.w = *w;
+  const int H = m->cfg.hidden;
+  AG_TRY(wmap(&L.tm_qkv, w->qkv_w, 3 * m->hq, H, "qkv_w"));
+  AG_TRY(wmap(&L.tm_out, w->out_w, H, m->hq, "out_w"));
+  AG_TRY(wmap(&L.tm_fc1, w->fc1_w, m->ffn_l, H, "fc1_w"));
+  AG_TRY(wmap(&L.tm_fc2, w->fc2_w, H, m->ffn_l, "fc2_w"));
+  L.ready = L.kpool != nullptr;
+  return AG_OK;
+}
+
+int32_t ag_model_set_kv_cache(ag_model* m, int32_t layer, void* k_pool, void* v_pool) {
+  if (!m || layer < 0 || layer >= m->cfg.num_layers || !k_pool || !v_pool) return fail(AG_EINVAL, "bad kv cache");
+  m->layers[layer].kpool = static_cast<bf16*>(k_pool);
+  m->layers[layer].vpool = static_cast<bf16*>(v_pool);
+  m->layers[layer].ready = m->layers[layer].w.qkv_w != nullptr;
+  return AG_OK;
+}
+
+int32_t ag_nccl_get_unique_id(void* out) {
+  if (!out) return fail(AG_EINVAL, "null");
+  if (!nccl().ok) return fail(AG_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  AG_TRY(check_nccl(nccl().GetUniqueId(&id), "ncclGetUniqueId"));
+  std::memcpy(out, &id, sizeof(id));
+  return AG_OK;
+}
+
+int32_t ag_model_init_tp(ag_model* m, const void* uid) {
+  if (!m || !uid) return fail(AG_EINVAL, "null");
+  if (m->cfg.tp_size == 1) return AG_OK;
+  if (!nccl().ok) return fail(AG_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  return check_nccl(nccl().CommInitRank(&m->comm, m->cfg.tp_size, id, m->cfg.tp_rank), "ncclCommInitRank");
+}
+
+int32_t ag_model_stage_step(ag_model* m, const ag_step* st, void* stream) {
+  if (!m || !st) return fail(AG_EINVAL, "null argument");
+  const ag_model_config& c = m->cfg;
+  const int S = st->num_tokens, B = st->num_seqs, NL = st->num_logits, bts = st->block_table_stride;
+  if (S < 0 || S > c.max_tokens) return fail(AG_EALLOC, "num_tokens exceeds max_tokens");
+  if (B < 0 || B > c.max_seqs) return fail(AG_EALLOC, "num_seqs exceeds max_seqs");
+  if (NL < 0 || NL > c.max_seqs) return fail(AG_EALLOC, "num_logits exceeds max_seqs");
+  if (bts < 1 || bts > c.max_blocks_per_seq) return fail(AG_EALLOC, "block_table_stride out of range");
+  for (int l = 0; l < c.num_layers; ++l)
+    if (!m->layers[l].ready) return fail(AG_EINVAL, "layer " + std::to_string(l) + " weights/kv not set");
+  if (!m->tok_emb) return fail(AG_EINVAL, "embeddings not set");
+  if (S > 0 && (!st->token_ids || !st->positions || !st->slot_mapping))
+    return fail(AG_EINVAL, "null token arrays");
+  if (!st->cu_q || !st->ctx_len || (B > 0 && !st->block_table) || (NL > 0 && !st->logit_rows))
+    return fail(AG_EINVAL, "null sequence arrays");
+  // validate the plan against capacities (the reference's EngineFault conditions)
+  if (st->cu_q[0] != 0 || st->cu_q[B] != S) return fail(AG_EFAULT, "cu_q must start at 0 and end at num_tokens");
+  for (int b = 0; b < B; ++b) {
+    const int q = st->cu_q[b + 1] - st->cu_q[b];
+    if (q < 0) return fail(AG_EFAULT, "cu_q not monotone");
+    const int kv = st->ctx_len[b] + q;
+    if (st->ctx_len[b] < 0 || (kv + c.block_size - 1) / c.block_size > bts)
+      return fail(AG_EFAULT, "sequence " + std::to_string(b) + " exceeds its block table");
+    for (int j = 0; j < (kv + c.block_size - 1) / c.block_size; ++j) {
+      const int blk = st->block_table[static_cast<size_t>(b) * bts + j];
+      if (blk < 0 || blk >= c.num_blocks) return fail(AG_EFAULT, "block id out of range");
+    }
+  }
+  for (int i = 0; i < S; ++i) {
+    const int s = st->slot_mapping[i];
+    if (s >= c.num_blocks * c.block_size) return fail(AG_EFAULT, "slot out of range");
+    if (st->positions[i] + 2 >= c.pos_rows || st->positions[i] < 0)
+      return fail(AG_EINVAL, "position beyond the position table");
+  }
+  for (int i = 0; i < NL; ++i)
+    if (st->logit_rows[i] < 0 || st->logit_rows[i] >= S) return fail(AG_EINVAL, "logit row out of range");
+
+  build_attention_work(st->cu_q, st->ctx_len, B, m->heads_l, m->part_cap, m->work);
+  // pack
+  uint8_t* h = m->meta_host;
+  size_t off = 0;
+  auto put = [&](const void* src, size_t bytes) -> size_t {
+    const size_t at = off;
+    if (bytes) std::memcpy(h + off, src, bytes);
+    off = align_up(off + bytes, 256);
+    return at;
+  };
+  const size_t o_ids = put(st->token_ids, sizeof(int32_t) * S);
+  const size_t o_pos = put(st->positions, sizeof(int32_t) * S);
+  const size_t o_slot = put(st->slot_mapping, sizeof(int32_t) * S);
+  const size_t o_cuq = put(st->cu_q, sizeof(int32_t) * (B + 1));
+  const size_t o_ctx = put(st->ctx_len, sizeof(int32_t) * B);
+  const size_t o_bt = put(st->block_table, sizeof(int32_t) * static_cast<size_t>(B) * bts);
+  const size_t o_lr = put(st->logit_rows, sizeof(int32_t) * NL);
+  const size_t need = off + align_up(sizeof(AttnItem) * m->work.items.size(), 256) +
+                      align_up(sizeof(AttnCombine) * m->work.combines.size(), 256);
+  if (need > m->meta_cap) return fail(AG_EALLOC, "metadata exceeds staging capacity");
+  const size_t o_items = put(m->work.items.data(), sizeof(AttnItem) * m->work.items.size());
+  const size_t o_comb = put(m->work.combines.data(), sizeof(AttnCombine) * m->work.combines.size());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  AG_CUDA(cudaMemcpyAsync(m->meta_dev, m->meta_host, off, cudaMemcpyHostToDevice, s));
+  const uint8_t* d = m->meta_dev;
+  m->d_ids = reinterpret_cast<const int32_t*>(d + o_ids);
+  m->d_pos = reinterpret_cast<const int32_t*>(d + o_pos);
+  m->d_slot = reinterpret_cast<const int32_t*>(d + o_slot);
+  m->d_cuq = reinterpret_cast<const int32_t*>(d + o_cuq);
+  m->d_ctx = reinterpret_cast<const int32_t*>(d + o_ctx);
+  m->d_bt = reinterpret_cast<const int32_t*>(d + o_bt);
+  m->d_lrows = reinterpret_cast<const int32_t*>(d + o_lr);
+  m->d_items = reinterpret_cast<const AttnItem*>(d + o_items);
+  m->d_comb = reinterpret_cast<const AttnCombine*>(d + o_comb);
+  m->S = S;
+  m->B = B;
+  m->n_logit = NL;
+  m->bt_stride = bts;
+  m->n_items = static_cast<int>(m->work.items.size());
+  m->n_comb = static_cast<int>(m->work.combines.size());
+  return AG_OK;
+}
+
+int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* logits_out, void* stream) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ag_model_config& c = m->cfg;
+  const int S = m->S, H = c.hidden;
+  const bool tp = c.tp_size > 1;
+  if (S > 0) {
+    AG_CUDA(ag::launch_embed(m->d_ids, m->d_pos, m->tok_emb, m->pos_emb, 2, S, H, c.vocab, c.pos_rows, m->resid, s));
+    const float qscale = 1.0f / std::sqrt(static_cast<float>(m->head_dim));
+    for (int l = 0; l < c.num_layers; ++l) {
+      const LayerState& L = m->layers[l];
+      const ag_layer_weights& w = L.w;
+      // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
+      if (tp && l > 0) {
+        AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(m->layers[l - 1].w.fc2_b), nullptr,
+                                     static_cast<const bf16*>(w.ln1_g), static_cast<const bf16*>(w.ln1_b), c.ln_eps, S,
+                                     H, m->xln, s));
+      } else {
+        AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln1_g),
+                                     static_cast<const bf16*>(w.ln1_b), c.ln_eps, S, H, m->xln, s));
+      }
+      // QKV projection: q -> qbuf (scaled), K/V -> paged cache slots
+      ag::GemmEpilogue ep;
+      ep.mode = ag::kEpiQkv;
+      ep.bias = static_cast<const bf16*>(w.qkv_b);
+      ep.out = m->qbuf;
+      ep.ldc = m->hq;
+      ep.hq = m->hq;
+      ep.q_scale = qscale;
+      ep.kcache = L.kpool;
+      ep.vcache = L.vpool;
+      ep.slot_mapping = m->d_slot;
+      ep.heads = m->heads_l;
+      ep.head_dim = m->head_dim;
+      ep.block_size = c.block_size;
+      AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s));
+      // mixed paged attention
+      ag::AttnParams ap;
+      ap.q = m->qbuf;
+      ap.ldq = m->hq;
+      ap.kcache = L.kpool;
+      ap.vcache = L.vpool;
+      ap.block_table = m->d_bt;
+      ap.bt_stride = m->bt_stride;
+      ap.cu_q = m->d_cuq;
+      ap.ctx_len = m->d_ctx;
+      ap.out = m->attn;
+      ap.ldo = m->hq;
+      ap.part_o = m->part_o;
+      ap.part_ml = m->part_ml;
+      ap.heads = m->heads_l;
+      ap.block_size = c.block_size;
+      AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_items, m->d_comb, m->n_comb, s));
+      // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
+      ag::GemmEpilogue eo;
+      eo.ldc = H;
+      if (!tp) {
+        eo.bias = static_cast<const bf16*>(w.out_b);
+        eo.residual = m->resid;
+        eo.ldr = H;
+        eo.out = m->resid;
+      } else {
+        eo.out = m->proj;
+      }
+      AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s));
+      if (tp) {
+        AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+        AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(w.out_b), nullptr,
+                                     static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps, S,
+                                     H, m->xln, s));
+      } else {
+        AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln2_g),
+                                     static_cast<const bf16*>(w.ln2_b), c.ln_eps, S, H, m->xln, s));
+      }
+      // FC1 + bias + ReLU
+      ag::GemmEpilogue e1;
+      e1.bias = static_cast<const bf16*>(w.fc1_b);
+      e1.relu = 1;
+      e1.out = m->ffn;
+      e1.ldc = m->ffn_l;
+      AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s));
+      // FC2 (+bias +residual / partial + all-reduce)
+      ag::GemmEpilogue e2;
+      e2.ldc = H;
+      if (!tp) {
+        e2.bias = static_cast<const bf16*>(w.fc2_b);
+        e2.residual = m->resid;
+        e2.ldr = H;
+        e2.out = m->resid;
+      } else {
+        e2.out = m->proj;
+      }
+      AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s));
+      if (tp) AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+    }
+    if (tp) {  // fold the last FC2 all-reduce into the residual stream
+      const ag_layer_weights& wl = m->layers[c.num_layers - 1].w;
+      AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(wl.fc2_b), nullptr, m->final_g,
+                                   m->final_b, c.ln_eps, S, H, m->xln, s));
+    }
+  }
+  const int NL = m->n_logit;
+  if (NL > 0) {
+    // final LayerNorm only on the rows that emit a token (logit skip)
+    AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H,
+                                 m->lm_in, s));
+    ag::GemmEpilogue el;
+    el.out = logits_out ? static_cast<void*>(logits_out) : static_cast<void*>(m->logits);
+    el.ldc = m->vocab_l;
+    el.out_f32 = 1;
+    float* lg = static_cast<float*>(el.out);
+    AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s));
+    if (!tp) {
+      AG_CUDA(ag::launch_argmax(lg, NL, m->vocab_l, m->vocab_l, 0, nullptr, out_tokens_dev, s));
+    } else {
+      AG_CUDA(ag::launch_argmax(lg, NL, m->vocab_l, m->vocab_l, m->vocab_off, m->cand_val, m->cand_idx, s));
+      AG_TRY(check_nccl(nccl().AllGather(m->cand_val, m->gathered_val, NL, ncclFloat32, m->comm, s), "allgather"));
+      AG_TRY(check_nccl(nccl().AllGather(m->cand_idx, m->gathered_idx, NL, ncclInt32, m->comm, s), "allgather"));
+      AG_CUDA(ag::launch_argmax_merge(m->gathered_val, m->gathered_idx, c.tp_size, NL, out_tokens_dev, s));
+    }
+  }
+  return AG_OK;
+}
+
+int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, float* logits_out, float* device_ms,
+                         void* stream) {
+  if (!m || !st) return fail(AG_EINVAL, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  AG_TRY(ag_model_stage_step(m, st, stream));
+  AG_CUDA(cudaEventRecord(m->ev0, s));
+  AG_TRY(ag_model_forward_staged(m, m->out_tok, logits_out, stream));
+  AG_CUDA(cudaEventRecord(m->ev1, s));
+  if (m->n_logit > 0)
+    AG_CUDA(cudaMemcpyAsync(m->tok_host, m->out_tok, sizeof(int32_t) * m->n_logit, cudaMemcpyDeviceToHost, s));
+  AG_CUDA(cudaStreamSynchronize(s));
+  if (device_ms) AG_CUDA(cudaEventElapsedTime(device_ms, m->ev0, m->ev1));
+  if (out_tokens && m->n_logit > 0) std::memcpy(out_tokens, m->tok_host, sizeof(int32_t) * m->n_logit);
+  return AG_OK;
+}
+
+// ---------------------------------------------------------------- standalone kernels
+int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias, const void* residual,
+                     int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32, int32_t M, int32_t N, int32_t K,
+                     int32_t block_n, void* stream) {
+  if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");
+  if (M < 0 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0) return fail(AG_EINVAL, "need N%32==0, K%8==0");
+  if (block_n == 0) block_n = ag::pick_block_n(M, N);
+  if (block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 128 or 256");
+  CUtensorMap ta, tb;
+  int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, 128);
+  if (r) return fail(AG_EINVAL, "tensor map A failed (alignment?)");
+  r = ag::make_tmap_kmajor(&tb, W, N, K, ldw, block_n);
+  if (r) return fail(AG_EINVAL, "tensor map W failed (alignment?)");
+  ag::GemmEpilogue ep;
+  ep.bias = static_cast<const bf16*>(bias);
+  ep.residual = static_cast<const bf16*>(residual);
+  ep.ldr = ldr;
+  ep.relu = relu;
+  ep.out = D;
+  ep.ldc = ldd;
+  ep.out_f32 = out_f32;
+  AG_CUDA(ag::launch_gemm(ta, tb, M, N, K, block_n, ep, 0, static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_kv_append(const void* k, const void* v, int32_t ld, const int32_t* slot_mapping, int32_t rows,
+                     int32_t heads, int32_t block_size, void* k_pool, void* v_pool, void* stream) {
+  if (!k || !v || !slot_mapping || !k_pool || !v_pool) return fail(AG_EINVAL, "null pointer");
+  AG_CUDA(ag::launch_kv_append(static_cast<const bf16*>(k), static_cast<const bf16*>(v), ld, slot_mapping, rows, heads,
+                               128, block_size, static_cast<bf16*>(k_pool), static_cast<bf16*>(v_pool),
+                               static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const void* v_pool,
+                           const int32_t* block_table_dev, int32_t bt_stride, const int32_t* cu_q_host,
+                           const int32_t* ctx_len_host, const int32_t* cu_q_dev, const int32_t* ctx_len_dev,
+                           int32_t num_seqs, int32_t heads, int32_t block_size, void* out, int32_t ldo,
+                           void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!q || !k_pool || !v_pool || !block_table_dev || !cu_q_host || !ctx_len_host || !out || !workspace)
+    return fail(AG_EINVAL, "null pointer");
+  if (block_size != 32) return fail(AG_EINVAL, "block_size must be 32");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // workspace: [items][combines][part_o][part_ml]
+  const int64_t row_bytes = static_cast<int64_t>(heads) * (128 + 2) * 4;
+  const int64_t meta_reserve = 1 << 20;
+  if (workspace_bytes < meta_reserve + row_bytes * 64) return fail(AG_EALLOC, "workspace too small");
+  const int part_cap = static_cast<int>((workspace_bytes - meta_reserve) / row_bytes);
+  AttnWork w;
+  build_attention_work(cu_q_host, ctx_len_host, num_seqs, heads, part_cap, w);
+  const size_t ib = sizeof(AttnItem) * w.items.size(), cb = sizeof(AttnCombine) * w.combines.size();
+  if (static_cast<int64_t>(align_up(ib, 256) + cb) > meta_reserve) return fail(AG_EALLOC, "too many attention items");
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  AG_CUDA(cudaMemcpyAsync(ws, w.items.data(), ib, cudaMemcpyHostToDevice, s));
+  AG_CUDA(cudaMemcpyAsync(ws + align_up(ib, 256), w.combines.data(), cb, cudaMemcpyHostToDevice, s));
+  ag::AttnParams ap;
+  ap.q = static_cast<const bf16*>(q);
+  ap.ldq = ldq;
+  ap.kcache = static_cast<const bf16*>(k_pool);
+  ap.vcache = static_cast<const bf16*>(v_pool);
+  ap.block_table = block_table_dev;
+  ap.bt_stride = bt_stride;
+  ap.cu_q = cu_q_dev;
+  ap.ctx_len = ctx_len_dev;
+  ap.out = static_cast<bf16*>(out);
+  ap.ldo = ldo;
+  ap.part_o = reinterpret_cast<float*>(ws + meta_reserve);
+  ap.part_ml = ap.part_o + static_cast<int64_t>(part_cap) * heads * 128;
+  ap.heads = heads;
+  ap.block_size = block_size;
+  AG_CUDA(ag::launch_attention(ap, reinterpret_cast<const AttnItem*>(ws),
+                               static_cast<int>(w.items.size()),
+                               reinterpret_cast<const AttnCombine*>(ws + align_up(ib, 256)),
+                               static_cast<int>(w.combines.size()), s));
+  // the host work vectors must outlive the async copies
+  AG_CUDA(cudaStreamSynchronize(s));
+  return AG_OK;
+}
+
+int32_t ag_layernorm(void* x, const void* delta, const void* delta_bias, const int32_t* row_index, const void* gamma,
+                     const void* beta, float eps, int32_t rows, int32_t hidden, void* out, void* stream) {
+  if (!x || !gamma || !beta || !out) return fail(AG_EINVAL, "null pointer");
+  AG_CUDA(ag::launch_layernorm(static_cast<bf16*>(x), static_cast<const bf16*>(delta),
+                               static_cast<const bf16*>(delta_bias), row_index, static_cast<const bf16*>(gamma),
+                               static_cast<const bf16*>(beta), eps, rows, hidden, static_cast<bf16*>(out),
+                               static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_embed_pos(const int32_t* ids, const int32_t* positions, const void* tok_emb, const void* pos_emb,
+                     int32_t pos_offset, int32_t rows, int32_t hidden, int32_t vocab, int32_t pos_rows, void* out,
+                     void* stream) {
+  if (!ids || !positions || !tok_emb || !pos_emb || !out) return fail(AG_EINVAL, "null pointer");
+  if (hidden % 8) return fail(AG_EINVAL, "hidden % 8 != 0");
+  AG_CUDA(ag::launch_embed(ids, positions, static_cast<const bf16*>(tok_emb), static_cast<const bf16*>(pos_emb),
+                           pos_offset, rows, hidden, vocab, pos_rows, static_cast<bf16*>(out),
+                           static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_argmax(const float* logits, int32_t rows, int32_t cols, int32_t ld, int32_t index_offset, float* out_val,
+                  int32_t* out_idx, void* stream) {
+  if (!logits || !out_idx) return fail(AG_EINVAL, "null pointer");
+  AG_CUDA(ag::launch_argmax(logits, rows, cols, ld, index_offset, out_val, out_idx, static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_kv_swap_out(const void* pool, const int32_t* block_ids_dev, int32_t n_blocks, int64_t block_elems,
+                       void* staging, void* stream) {
+  if (!pool || !block_ids_dev || !staging) return fail(AG_EINVAL, "null pointer");
+  AG_CUDA(ag::launch_block_copy(static_cast<const bf16*>(pool), static_cast<bf16*>(staging), block_ids_dev, n_blocks,
+                                block_elems, true, static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_kv_swap_in(const void* staging, const int32_t* block_ids_dev, int32_t n_blocks, int64_t block_elems,
+                      void* pool, void* stream) {
+  if (!pool || !block_ids_dev || !staging) return fail(AG_EINVAL, "null pointer");
+  AG_CUDA(ag::launch_block_copy(static_cast<const bf16*>(staging), static_cast<bf16*>(pool), block_ids_dev, n_blocks,
+                                block_elems, false, static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// Internal (C++) declarations shared by the kernel translation units and the C-ABI layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ag {
+
+enum EpiMode : int { kEpiPlain = 0, kEpiQkv = 1 };
+
+struct GemmEpilogue {
+  int mode = kEpiPlain;
+  const __nv_bfloat16* bias = nullptr;      // [N] or null
+  const __nv_bfloat16* residual = nullptr;  // [M, ldr] or null (plain mode)
+  int ldr = 0;
+  int relu = 0;
+  void* out = nullptr;  // bf16 (or f32 when out_f32) [M, ldc]; q output in QKV mode
+  int ldc = 0;
+  int out_f32 = 0;
+  // QKV mode: columns [0,hq) -> q (scaled), [hq,2hq) -> K cache, [2hq,3hq) -> V cache
+  int hq = 0;
+  float q_scale = 1.0f;
+  __nv_bfloat16* kcache = nullptr;  // [num_blocks, heads, block_size, head_dim]
+  __nv_bfloat16* vcache = nullptr;
+  const int32_t* slot_mapping = nullptr;  // [M]; <0 = skip
+  int heads = 0;
+  int head_dim = 128;
+  int block_size = 32;
+};
+
+int make_tmap_kmajor(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld_elems,
+                     int box_rows);
+int num_sms();
+int pick_block_n(int M, int N);
+cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
+                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream);
+
+// embed: out[r] = tok_emb[ids[r]] + pos_emb[positions[r] + pos_offset]
+cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,
+                         const __nv_bfloat16* pos_emb, int pos_offset, int rows, int hidden,
+                         int vocab, int max_pos_rows, __nv_bfloat16* out, cudaStream_t stream);
+
+// layernorm over rows of x (optionally gathered through row_index), fp32 statistics.
+// If delta != null: x[r] = x[r] + delta[r] (+ delta_bias) is written back first (residual add).
+cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta,
+                             const __nv_bfloat16* delta_bias, const int32_t* row_index,
+                             const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps,
+                             int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream);
+
+// standalone paged KV append: k/v rows [rows, heads*head_dim] -> cache slots
+cudaError_t launch_kv_append(const __nv_bfloat16* k, const __nv_bfloat16* v, int ld_src,
+                             const int32_t* slot_mapping, int rows, int heads, int head_dim,
+                             int block_size, __nv_bfloat16* kcache, __nv_bfloat16* vcache,
+                             cudaStream_t stream);
+
+// Work item of the mixed paged attention (host-built).
+struct AttnItem {
+  int32_t seq;        // sequence index
+  int32_t q_start;    // first query row inside the sequence's q chunk
+  int32_t q_rows;     // rows of this tile (<= 64)
+  int32_t kv_start;   // first kv position (inclusive)
+  int32_t kv_end;     // last kv position (exclusive), already clipped by causality
+  int32_t part_row;   // >=0: row base into the split-KV partial buffers; -1: write final output
+  int32_t pad0, pad1;
+};
+
+struct AttnCombine {
+  int32_t tok_row;    // global token row of the first row of the tile
+  int32_t q_rows;
+  int32_t first_part; // part_row of split 0
+  int32_t n_splits;   // splits are laid out part_row = first_part + s * q_rows
+};
+
+struct AttnParams {
+  const __nv_bfloat16* q;  // [S_f, heads*head_dim] (already scaled)
+  int ldq;
+  const __nv_bfloat16* kcache;
+  const __nv_bfloat16* vcache;
+  const int32_t* block_table;  // [B, bt_stride]
+  int bt_stride;
+  const int32_t* cu_q;     // [B+1]
+  const int32_t* ctx_len;  // [B] cached prefix length before this step
+  __nv_bfloat16* out;      // [S_f, heads*head_dim]
+  int ldo;
+  float* part_o;           // [P, heads, head_dim]
+  float* part_ml;          // [P, heads, 2]
+  int heads;
+  int block_size;
+};
+
+cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_items,
+                             const AttnCombine* combines, int n_combines, cudaStream_t stream);
+
+// argmax over rows of logits (f32), optional vocab offset; writes (value, index) pairs
+cudaError_t launch_argmax(const float* logits, int rows, int cols, int ld, int index_offset,
+                          float* out_val, int32_t* out_idx, cudaStream_t stream);
+
+// merge per-rank (value,index) candidates [tp, rows] -> index [rows]
+cudaError_t launch_argmax_merge(const float* vals, const int32_t* idx, int tp, int rows,
+                                int32_t* out_idx, cudaStream_t stream);
+
+// gather block rows: dst[i] = src[index[i]] (bf16 rows of width cols)
+cudaError_t launch_gather_rows(const __nv_bfloat16* src, int ld_src, const int32_t* index, int rows,
+                               int cols, __nv_bfloat16* dst, int ld_dst, cudaStream_t stream);
+
+// KV block swap: gather=true copies pool[block_ids[i]] -> dst[i] (contiguous staging);
+// gather=false copies src[i] -> dst[block_ids[i]] (staging back into the pool).
+cudaError_t launch_block_copy(const __nv_bfloat16* src, __nv_bfloat16* dst, const int32_t* block_ids,
+                              int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream);
+
+}  // namespace ag

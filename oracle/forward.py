@@ -29,8 +29,13 @@ POS_OFFSET = 2
 HEAD_DIM = 128
 
 
+ROUND_BF16 = True  # False = pure fp32 restatement (used to pin against transformers' fp32 OPT)
+
+
 def rb(x: torch.Tensor) -> torch.Tensor:
     """Round to bf16 and return as fp32 (a storage point of the device pipeline)."""
+    if not ROUND_BF16:
+        return x
     return x.to(torch.bfloat16).to(torch.float32)
 
 
@@ -114,7 +119,8 @@ class OracleOPT:
         self.allreduce = allreduce
         heads_l = cfg.num_heads // tp_size
         self.heads_l = heads_l
-        self.k_pools = [torch.zeros(num_blocks, heads_l, block_size, HEAD_DIM, dtype=torch.bfloat16)
+        pool_dtype = torch.bfloat16 if ROUND_BF16 else torch.float32
+        self.k_pools = [torch.zeros(num_blocks, heads_l, block_size, HEAD_DIM, dtype=pool_dtype)
                         for _ in range(cfg.num_layers)]
         self.v_pools = [torch.zeros_like(p) for p in self.k_pools]
         self.scale = 1.0 / math.sqrt(HEAD_DIM)

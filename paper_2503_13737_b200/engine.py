@@ -1,0 +1,480 @@
+"""Iteration loop with the GPU forward behind an Executor.
+
+step(): admit arrivals -> order_queue -> policy plan -> swap-out / KV allocation ->
+``executor.execute(batch)`` -> advance the clock -> emit tokens -> release / re-enqueue.
+
+The only departure from the reference engine is the clock advance.  SPEC.md:484 advances the
+clock by ``iteration_time(S_f)``; here the clock source is selectable:
+
+  clock="virtual"  iteration_time(S_f) from the cost model (bit-exact scheduler parity with the
+                   CPU oracle run; the device still executes every plan),
+  clock="device"   CUDA-event time of the forward measured by the executor,
+  clock="wall"     host wall time of executor.execute (packing + H2D + forward + D2H).
+
+Pinned decisions: a prompt's final chunk emits the first output token (so a
+request takes N_chunks + output_len - 1 iterations and output_len emissions, SPEC.md:429-437
+and the token-conservation invariant :510); TTFT is taken at the end of that iteration
+(:518); an empty plan advances the clock to min(next arrival, now + T_max) (:519).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import asdict, dataclass, field
+from typing import Protocol
+
+import numpy as np
+
+from .cost_model import ModelProfile, iteration_time
+from .errors import AllocationError, EngineFault, StateError
+from .kvc import BlockPool
+from .policies import BatchPlan, PlanContext, PolicyConfig, Selection, has_prompt_left, plan as make_plan
+from .sched_core import (ChunkStats, Phase, QueueEntry, jct_allowance, jct_initial_estimate, order_queue,
+                         propagate_debt)
+from .workload import RequestSpec, SLOKind
+
+CSV_COLUMNS = ("policy", "tokens_per_s", "reqs_per_s", "goodput", "slo_attainment", "jct_slo_attainment",
+               "jct_mean", "jct_p5", "jct_p95", "gpu_util_mean", "kvc_util_mean", "preemptions", "truncated")
+
+
+# ----------------------------------------------------------------------------- device batch
+def synthetic_tokens(request_id: int, positions: np.ndarray, vocab: int) -> np.ndarray:
+    """Deterministic token ids in [4, vocab) keyed by (request, position) (splitmix64)."""
+    x = (np.uint64(request_id) << np.uint64(32)) ^ positions.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return (np.uint64(4) + x % np.uint64(vocab - 4)).astype(np.int32)
+
+
+@dataclass
+class DeviceBatch:
+    """Packed BatchPlan for one forward (the C-ABI ag_step)."""
+    request_ids: list[int]
+    token_ids: np.ndarray     # int32 [S_f]
+    positions: np.ndarray     # int32 [S_f]
+    cu_q: np.ndarray          # int32 [B+1]
+    ctx_len: np.ndarray       # int32 [B]
+    block_table: np.ndarray   # int32 [B, stride]
+    slot_mapping: np.ndarray  # int32 [S_f]
+    logit_rows: np.ndarray    # int32 [n_logit]
+    logit_request_ids: list[int]
+
+    @property
+    def num_tokens(self) -> int:
+        return int(self.token_ids.shape[0])
+
+    def h2d_bytes(self) -> int:
+        return sum(a.nbytes for a in (self.token_ids, self.positions, self.cu_q, self.ctx_len, self.block_table,
+                                      self.slot_mapping, self.logit_rows))
+
+    def seq_shapes(self) -> list[tuple[int, int]]:
+        """(q_i, p_i) per sequence for roofline accounting."""
+        q = np.diff(self.cu_q)
+        return [(int(a), int(b)) for a, b in zip(q, self.ctx_len)]
+
+
+@dataclass
+class StepResult:
+    token_ids: np.ndarray  # int32 [n_logit] greedy next tokens
+    elapsed_s: float       # time charged to the clock by clock="device"
+    device_s: float = 0.0
+    wall_s: float = 0.0
+    logits: object = None  # optional fp32 [n_logit, V] (parity mode)
+
+
+class Executor(Protocol):
+    max_tokens: int
+    max_seqs: int
+    vocab: int
+
+    def execute(self, batch: DeviceBatch) -> StepResult: ...
+
+    def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None: ...
+
+    def swap_in(self, request_id: int, block_ids: list[int], tokens: int) -> None: ...
+
+
+class VirtualExecutor:
+    """No device: the reference simulator's behaviour (clock from the cost model only)."""
+
+    def __init__(self, vocab: int = 50272, max_tokens: int = 1 << 30, max_seqs: int = 1 << 30):
+        self.vocab, self.max_tokens, self.max_seqs = vocab, max_tokens, max_seqs
+
+    def execute(self, batch: DeviceBatch) -> StepResult:
+        return StepResult(token_ids=np.zeros(len(batch.logit_rows), np.int32), elapsed_s=0.0)
+
+    def swap_out(self, request_id, block_ids, tokens):
+        pass
+
+    def swap_in(self, request_id, block_ids, tokens):
+        pass
+
+
+# ----------------------------------------------------------------------------- metrics
+@dataclass
+class RequestRecord:
+    spec: RequestSpec
+    prompt_done: int = 0
+    generated: int = 0
+    first_token_time: float | None = None
+    emit_times: list[float] = field(default_factory=list)
+    completion_time: float | None = None
+    preempt_time: float | None = None
+    tokens_out: list[int] = field(default_factory=list)
+    chunks: list[int] = field(default_factory=list)
+
+    def events_met(self) -> tuple[int, int]:
+        """(met, total) iteration-level token events (TTFT + each TBT gap) of an online request."""
+        slo = self.spec.slo
+        if slo.kind is SLOKind.OFFLINE or not self.emit_times:
+            return 0, 0
+        met = int(self.emit_times[0] - self.spec.arrival_time <= slo.ttft_slo + 1e-12)
+        for a, b in zip(self.emit_times, self.emit_times[1:]):
+            met += int(b - a <= slo.tbt_slo + 1e-12)
+        return met, len(self.emit_times)
+
+    def good(self) -> bool:
+        if self.completion_time is None:
+            return False
+        slo = self.spec.slo
+        if slo.kind is SLOKind.OFFLINE:
+            return self.completion_time - self.spec.arrival_time <= slo.jct_slo + 1e-12
+        met, total = self.events_met()
+        return met == total
+
+
+@dataclass
+class IterationRecord:
+    index: int
+    start: float
+    elapsed: float
+    forward_size: int
+    token_budget: int
+    num_seqs: int
+    num_decode: int
+    allocated_tokens: int
+    preemptions: int
+    device_s: float = 0.0
+    wall_s: float = 0.0
+    events: int = 0
+    events_met: int = 0
+    slo_tokens: int = 0   # tokens of this forward whose request met (or is on track for) its deadline
+
+
+@dataclass
+class MetricsReport:
+    policy: str
+    tokens_per_s: float
+    reqs_per_s: float
+    goodput: float
+    slo_attainment: float
+    jct_slo_attainment: float
+    jct_mean: float
+    jct_p5: float
+    jct_p95: float
+    gpu_util_mean: float
+    kvc_util_mean: float
+    preemptions: int
+    truncated: bool
+    goodput_windowed: float = 0.0
+    slo_tokens_per_s: float = 0.0
+    makespan: float = 0.0
+    iterations: int = 0
+    completed: int = 0
+
+    def csv_row(self) -> str:
+        vals = [getattr(self, c) for c in CSV_COLUMNS]
+        return ",".join(str(v) if not isinstance(v, float) else repr(v) for v in vals)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+class MetricsAccumulator:
+    def __init__(self):
+        self.requests: dict[int, RequestRecord] = {}
+        self.iterations: list[IterationRecord] = []
+        self.total_blocks_tokens = 1
+
+
+def compute_metrics(acc: MetricsAccumulator, policy: str, truncated: bool, window_s: float = 1.0) -> MetricsReport:
+    """SPEC.md:499-507 metric definitions over a finished (or truncated) run."""
+    recs = list(acc.requests.values())
+    done = [r for r in recs if r.completion_time is not None]
+    if not recs or not acc.iterations:
+        return MetricsReport(policy, 0.0, 0.0, 0.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, truncated)
+    t0 = min(r.spec.arrival_time for r in recs)
+    t_end = max([r.completion_time for r in done] + [acc.iterations[-1].start + acc.iterations[-1].elapsed])
+    makespan = max(t_end - t0, 1e-12)
+    tokens = sum(r.prompt_done + r.generated for r in recs)
+    met = tot = 0
+    for r in recs:
+        m, t = r.events_met()
+        met += m
+        tot += t
+    good = [r for r in done if r.good()]
+    offline = [r for r in done if r.spec.slo.kind is SLOKind.OFFLINE]
+    jcts = np.array([r.completion_time - r.spec.arrival_time for r in done]) if done else np.zeros(1)
+    n_win = max(1, math.ceil(makespan / window_s))
+    per_win = np.zeros(n_win)
+    for r in good:
+        per_win[min(n_win - 1, int((r.completion_time - t0) / window_s))] += 1
+    busy = [it for it in acc.iterations if it.forward_size > 0]
+    return MetricsReport(
+        policy=policy,
+        tokens_per_s=tokens / makespan,
+        reqs_per_s=len(done) / makespan,
+        goodput=len(good) / makespan,
+        slo_attainment=met / tot if tot else 1.0,
+        jct_slo_attainment=(sum(r.good() for r in offline) / len(offline)) if offline else 1.0,
+        jct_mean=float(jcts.mean()),
+        jct_p5=float(np.percentile(jcts, 5)),
+        jct_p95=float(np.percentile(jcts, 95)),
+        gpu_util_mean=float(np.mean([it.forward_size / it.token_budget for it in busy])) if busy else 0.0,
+        kvc_util_mean=float(np.mean([it.allocated_tokens / acc.total_blocks_tokens for it in busy])) if busy else 0.0,
+        preemptions=sum(it.preemptions for it in acc.iterations),
+        truncated=truncated,
+        goodput_windowed=float(per_win.mean() / window_s),
+        slo_tokens_per_s=sum(r.spec.prompt_len + r.spec.output_len for r in good) / makespan,
+        makespan=makespan,
+        iterations=len(acc.iterations),
+        completed=len(done),
+    )
+
+
+# ----------------------------------------------------------------------------- engine
+class Engine:
+    """Deterministic single-threaded loop; the BlockPool is single-writer."""
+
+    def __init__(self, trace: list[RequestSpec], profile: ModelProfile, policy: PolicyConfig | None = None,
+                 executor: Executor | None = None, *, clock: str = "virtual", kv_blocks: int | None = None,
+                 block_size: int = 32, horizon_s: float = math.inf, per_token_swap_cost_s: float = 0.0,
+                 check_invariants: bool = False):
+        if clock not in ("virtual", "device", "wall"):
+            raise ValueError(f"unknown clock {clock!r}")
+        self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
+        self.profile = profile
+        self.cfg = policy or PolicyConfig()
+        self.executor = executor or VirtualExecutor()
+        self.clock_mode = clock
+        blocks = kv_blocks if kv_blocks is not None else profile.kvc_capacity_tokens // block_size
+        self.pool = BlockPool(max(1, blocks), block_size)
+        self.stats = ChunkStats(avg_chunk_len=float(profile.pivot_forward_size),
+                                t_max=iteration_time(profile.pivot_forward_size, profile))
+        self.clock = 0.0
+        self.horizon = horizon_s
+        self.swap_cost = per_token_swap_cost_s
+        self.check = check_invariants
+        self.queue: list[QueueEntry] = []
+        self.long_active: set[int] = set()
+        self.metrics = MetricsAccumulator()
+        self.metrics.total_blocks_tokens = self.pool.total_blocks * block_size
+        self._next_arrival = 0
+        self._stamp = 0
+        self.plans: list[BatchPlan] = []      # kept for parity tests (scheduler decisions)
+        self.tables: list[dict] = []          # per-step block tables (physical ids)
+        self.keep_history = False
+
+    # -------------------------------------------------------------- helpers
+    def _stamp_next(self) -> int:
+        self._stamp += 1
+        return self._stamp
+
+    def _admit(self) -> None:
+        while self._next_arrival < len(self.trace) and self.trace[self._next_arrival].arrival_time <= self.clock:
+            spec = self.trace[self._next_arrival]
+            self._next_arrival += 1
+            e = QueueEntry(request=spec, phase=Phase.PROMPT_PENDING, remaining_prompt_tokens=spec.prompt_len,
+                           seq_len=0, enqueue_time=spec.arrival_time, is_long=spec.is_long(), seq=self._stamp_next())
+            if e.is_offline:
+                e.iter_allowance = jct_allowance(spec, jct_initial_estimate(spec, self.stats), self.stats)
+            self.queue.append(e)
+            self.metrics.requests[spec.id] = RequestRecord(spec)
+
+    def done(self) -> bool:
+        return self._next_arrival >= len(self.trace) and not self.queue
+
+    # -------------------------------------------------------------- one iteration
+    def step(self) -> IterationRecord | None:
+        self._admit()
+        if not self.queue:
+            if self._next_arrival < len(self.trace):
+                self.clock = max(self.clock, self.trace[self._next_arrival].arrival_time)
+            return None
+        self.queue = order_queue(self.queue, self.clock, self.stats)
+        ctx = PlanContext(self.pool, self.stats, self.profile, self.clock, set(self.long_active))
+        plan = make_plan(self.queue, ctx, self.cfg)
+        plan.check()
+        if plan.forward_size > self.executor.max_tokens or len(plan.selections) > self.executor.max_seqs:
+            raise EngineFault(f"plan of {plan.forward_size} tokens / {len(plan.selections)} sequences exceeds the "
+                              f"executor capacity ({self.executor.max_tokens}/{self.executor.max_seqs})")
+        start = self.clock
+        by_id = {e.request_id: e for e in self.queue}
+
+        # ---- preemptions (swap out) before allocation
+        swap_tokens = 0
+        for rid in plan.preempted:
+            e = by_id[rid]
+            tokens, table = self.pool.preempt_with_table(rid)
+            self.executor.swap_out(rid, table, tokens)
+            swap_tokens += tokens
+            self.stats.observe_preemption()
+            rec = self.metrics.requests[rid]
+            rec.preempt_time = start
+            e.phase = Phase.PREEMPTED
+            e.enqueue_time = start
+            e.seq = self._stamp_next()
+
+        if not plan.selections:
+            nxt = self.trace[self._next_arrival].arrival_time if self._next_arrival < len(self.trace) else math.inf
+            self.clock = min(nxt, self.clock + self.stats.t_max)
+            return None
+
+        # ---- allocation + batch packing
+        free_before = self.pool.free_blocks
+        rows_tok, rows_pos, rows_slot, cu, ctx_len, tables, logit_rows, logit_ids = [], [], [], [0], [], [], [], []
+        for sel in plan.selections:
+            e = by_id[sel.request_id]
+            rid = sel.request_id
+            try:
+                if rid in self.pool.swapped_out:
+                    saved = self.pool.swapped_out[rid]
+                    self.pool.allocate(rid, self.pool.demand_readmit(rid))
+                    self.executor.swap_in(rid, self.pool.block_table(rid), saved)
+                    swap_tokens += saved
+                    rec = self.metrics.requests[rid]
+                    if rec.preempt_time is not None:
+                        self.stats.observe_preemption_duration(start - rec.preempt_time)
+                prompt = has_prompt_left(e)
+                before = self.pool.tokens_stored(rid)
+                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if prompt else self.pool.demand_tg(rid))
+                self.pool.allocate(rid, demand)
+            except (AllocationError, StateError) as exc:
+                raise EngineFault(f"plan infeasible against the pool: {exc}") from exc
+            pos = np.arange(before, before + sel.chunk_len, dtype=np.int32)
+            rows_pos.append(pos)
+            rows_tok.append(synthetic_tokens(rid, pos, self.executor.vocab))
+            rows_slot.append(np.asarray(self.pool.slots(rid, before, sel.chunk_len), dtype=np.int32))
+            ctx_len.append(before)
+            cu.append(cu[-1] + sel.chunk_len)
+            tables.append(self.pool.block_table(rid))
+            if sel.is_final_chunk:
+                logit_rows.append(cu[-1] - 1)
+                logit_ids.append(rid)
+        if free_before - self.pool.free_blocks != plan.blocks_needed:
+            raise EngineFault(f"allocated {free_before - self.pool.free_blocks} blocks, plan expected "
+                              f"{plan.blocks_needed}")
+        stride = max(len(t) for t in tables)
+        bt = np.zeros((len(tables), stride), dtype=np.int32)
+        for i, t in enumerate(tables):
+            bt[i, :len(t)] = t
+        batch = DeviceBatch(request_ids=[s.request_id for s in plan.selections], token_ids=np.concatenate(rows_tok),
+                            positions=np.concatenate(rows_pos), cu_q=np.asarray(cu, dtype=np.int32),
+                            ctx_len=np.asarray(ctx_len, dtype=np.int32), block_table=bt,
+                            slot_mapping=np.concatenate(rows_slot), logit_rows=np.asarray(logit_rows, dtype=np.int32),
+                            logit_request_ids=logit_ids)
+        if self.check:
+            self.pool.check_conservation()
+        if self.keep_history:
+            self.plans.append(plan)
+            self.tables.append({rid: list(row[:len(t)]) for rid, row, t in zip(batch.request_ids, bt, tables)})
+
+        # ---- execute and advance the clock
+        t_host = time.perf_counter()
+        res = self.executor.execute(batch)
+        wall = time.perf_counter() - t_host
+        if self.clock_mode == "virtual":
+            elapsed = iteration_time(plan.forward_size, self.profile)
+        elif self.clock_mode == "device":
+            elapsed = res.elapsed_s
+        else:
+            elapsed = wall
+        elapsed += swap_tokens * self.swap_cost
+        self.clock = start + elapsed
+        now = self.clock
+
+        # ---- emission, statistics, re-enqueue
+        it = IterationRecord(index=len(self.metrics.iterations), start=start, elapsed=elapsed,
+                             forward_size=plan.forward_size, token_budget=plan.token_budget,
+                             num_seqs=len(plan.selections), num_decode=0,
+                             allocated_tokens=self.pool.allocated_tokens, preemptions=len(plan.preempted),
+                             device_s=res.device_s, wall_s=wall)
+        tok_by_id = dict(zip(logit_ids, res.token_ids.tolist()))
+        selected = set()
+        finished = []
+        for sel in plan.selections:
+            e = by_id[sel.request_id]
+            rid = sel.request_id
+            selected.add(rid)
+            rec = self.metrics.requests[rid]
+            spec = rec.spec
+            if e.is_offline:
+                propagate_debt(e, start - e.enqueue_time)
+            prompt = has_prompt_left(e)
+            if prompt:
+                self.stats.observe_chunk(sel.chunk_len)
+                rec.prompt_done += sel.chunk_len
+                rec.chunks.append(sel.chunk_len)
+                e.remaining_prompt_tokens -= sel.chunk_len
+                e.seq_len += sel.chunk_len
+                if e.is_long:
+                    self.long_active.add(rid)
+            else:
+                self.stats.observe_tg_step()
+                it.num_decode += 1
+                e.seq_len += 1
+            if not sel.is_final_chunk:
+                # non-final chunk: same TTFT clock, back in the queue
+                on_track = spec.slo.kind is SLOKind.OFFLINE or now - spec.arrival_time <= spec.slo.ttft_slo
+                it.slo_tokens += sel.chunk_len if on_track else 0
+                e.phase = Phase.PROMPT_PENDING
+                e.seq = self._stamp_next()
+                continue
+            if prompt and e.is_long:
+                self.long_active.discard(rid)
+            # token event
+            prev = rec.emit_times[-1] if rec.emit_times else None
+            rec.emit_times.append(now)
+            rec.generated += 1
+            rec.tokens_out.append(tok_by_id.get(rid, -1))
+            if rec.first_token_time is None:
+                rec.first_token_time = now
+            if spec.slo.kind is SLOKind.ONLINE:
+                it.events += 1
+                ok = (now - spec.arrival_time <= spec.slo.ttft_slo + 1e-12) if prev is None else (
+                    now - prev <= spec.slo.tbt_slo + 1e-12)
+                it.events_met += int(ok)
+                it.slo_tokens += sel.chunk_len if ok else 0
+            else:
+                it.slo_tokens += sel.chunk_len if now - spec.arrival_time <= spec.slo.jct_slo else 0
+            if rec.generated >= spec.output_len:
+                rec.completion_time = now
+                self.pool.release(rid)
+                finished.append(rid)
+            else:
+                e.phase = Phase.TG_READY
+                e.remaining_prompt_tokens = 0
+                e.enqueue_time = now
+                e.seq = self._stamp_next()
+        if finished:
+            gone = set(finished)
+            self.queue = [e for e in self.queue if e.request_id not in gone]
+        self.metrics.iterations.append(it)
+        return it
+
+    def run(self, max_steps: int | None = None) -> MetricsReport:
+        truncated = False
+        steps = 0
+        while not self.done():
+            if self.clock > self.horizon:
+                truncated = True
+                break
+            if max_steps is not None and steps >= max_steps:
+                truncated = True
+                break
+            if self.step() is not None:
+                steps += 1
+        return compute_metrics(self.metrics, self.cfg.policy, truncated)

@@ -1,0 +1,163 @@
+"""CudaExecutor: runs each packed BatchPlan on the B200 through libaccelgen_b200.so.
+
+Replaces the reference's "advance clock by iteration_time(S_f)" with a real
+forward.  Ownership follows SURVEY §8b: weights and the KV pool are allocated once here (torch
+is used only as the device allocator), the scheduler owns block-id assignment, metadata is
+packed into pinned memory and copied H2D by the library each step, next-token ids come back
+D2H.  There is no CPU fallback: without CUDA or the library this raises EngineFault.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from .engine import DeviceBatch, StepResult
+from .errors import EngineFault
+from .model import HEAD_DIM, OPTConfig, init_weights
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class CudaExecutor:
+    def __init__(self, cfg: OPTConfig, num_blocks: int, *, max_tokens: int = 4096, max_seqs: int = 512,
+                 max_blocks_per_seq: int | None = None, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
+                 init: str = "opt", weights: dict | None = None, device: int | None = None,
+                 parity_logits: bool = False, nccl_uid: bytes | None = None):
+        if not torch.cuda.is_available():
+            raise EngineFault("CudaExecutor needs a CUDA device (no CPU fallback)")
+        self.lib = _lib.load()
+        self.cfg = cfg
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.vocab = cfg.vocab
+        self.max_tokens, self.max_seqs = max_tokens, max_seqs
+        self.block_size = 32
+        self.num_blocks = num_blocks
+        self.max_blocks_per_seq = max_blocks_per_seq or (cfg.pos_rows + self.block_size - 1) // self.block_size
+        self.parity_logits = parity_logits
+        heads_l = cfg.num_heads // tp_size
+        self.heads_l = heads_l
+
+        w = weights if weights is not None else init_weights(cfg, seed, self.device, tp_rank, tp_size, init)
+        self.w = self._to_device(w)
+        # one KV allocation for every layer: [L, 2, blocks, heads_l, 32, 128] bf16, zero-filled so
+        # never-written slots hold finite values
+        self.kv = torch.zeros(cfg.num_layers, 2, num_blocks, heads_l, self.block_size, HEAD_DIM,
+                              dtype=torch.bfloat16, device=self.device)
+
+        mc = _lib.ModelConfig(hidden=cfg.hidden, num_layers=cfg.num_layers, num_heads=cfg.num_heads, ffn=cfg.ffn,
+                              vocab=cfg.vocab, pos_rows=cfg.pos_rows, tp_rank=tp_rank, tp_size=tp_size,
+                              num_blocks=num_blocks, block_size=self.block_size, max_tokens=max_tokens,
+                              max_seqs=max_seqs, max_blocks_per_seq=self.max_blocks_per_seq, ln_eps=cfg.ln_eps)
+        handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.ag_model_create(C.byref(mc), C.byref(handle)))
+        self.handle = handle
+        ww = self.w
+        _lib.check(self.lib.ag_model_set_embeddings(handle, ww["tok_emb"].data_ptr(), ww["pos_emb"].data_ptr(),
+                                                    ww["final_g"].data_ptr(), ww["final_b"].data_ptr()))
+        for l, L in enumerate(ww["layers"]):
+            lw = _lib.LayerWeights(*[L[name].data_ptr() for name, _ in _lib.LayerWeights._fields_])
+            _lib.check(self.lib.ag_model_set_layer(handle, l, C.byref(lw)))
+            _lib.check(self.lib.ag_model_set_kv_cache(handle, l, self.kv[l, 0].data_ptr(), self.kv[l, 1].data_ptr()))
+        if tp_size > 1:
+            if nccl_uid is None:
+                raise EngineFault("tp_size > 1 needs the NCCL unique id broadcast by rank 0")
+            buf = C.create_string_buffer(bytes(nccl_uid), 128)
+            _lib.check(self.lib.ag_model_init_tp(handle, buf))
+        self._dev_ms = C.c_float(0.0)
+        self._swapped: dict[int, torch.Tensor] = {}
+        self.logits_buf = torch.empty(max_seqs, cfg.vocab // tp_size, dtype=torch.float32, device=self.device) \
+            if parity_logits else None
+        self.steps = 0
+        self.launches_per_step = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _lib.load()
+        buf = C.create_string_buffer(128)
+        _lib.check(lib.ag_nccl_get_unique_id(buf))
+        return buf.raw
+
+    def _to_device(self, w: dict) -> dict:
+        def mv(t):
+            return t.to(self.device, torch.bfloat16).contiguous()
+        out = {k: mv(v) for k, v in w.items() if k != "layers"}
+        out["layers"] = [{k: mv(v) for k, v in L.items()} for L in w["layers"]]
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.ag_model_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- step
+    def make_step(self, b: DeviceBatch) -> tuple[_lib.Step, list[np.ndarray]]:
+        arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in
+                (b.token_ids, b.positions, b.cu_q, b.ctx_len, b.block_table, b.slot_mapping, b.logit_rows)]
+        ids, pos, cu, ctx, bt, slot, lr = arrs
+        st = _lib.Step(num_tokens=ids.shape[0], num_seqs=ctx.shape[0], num_logits=lr.shape[0],
+                       block_table_stride=bt.shape[1] if bt.ndim == 2 and bt.shape[1] > 0 else 1,
+                       token_ids=_np_ptr(ids), positions=_np_ptr(pos), cu_q=_np_ptr(cu), ctx_len=_np_ptr(ctx),
+                       block_table=_np_ptr(bt), slot_mapping=_np_ptr(slot), logit_rows=_np_ptr(lr))
+        return st, arrs
+
+    def execute(self, batch: DeviceBatch) -> StepResult:
+        st, keep = self.make_step(batch)
+        n = int(batch.logit_rows.shape[0])
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        logits_ptr = self.logits_buf.data_ptr() if self.logits_buf is not None else None
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        t0 = time.perf_counter()
+        _lib.check(self.lib.ag_model_forward(self.handle, C.byref(st), _np_ptr(out), logits_ptr,
+                                             C.byref(self._dev_ms), stream))
+        wall = time.perf_counter() - t0
+        del keep
+        self.steps += 1
+        logits = self.logits_buf[:n].cpu() if self.logits_buf is not None else None
+        dev_s = self._dev_ms.value / 1e3
+        return StepResult(token_ids=out[:n].copy(), elapsed_s=dev_s, device_s=dev_s, wall_s=wall, logits=logits)
+
+    # ---------------------------------------------------------------- preemption swap (kvc.py:153-160)
+    def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
+        if not block_ids:
+            return
+        ids = torch.tensor(block_ids, dtype=torch.int32, device=self.device)
+        n = len(block_ids)
+        stage = torch.empty(self.cfg.num_layers, 2, n, self.heads_l, self.block_size, HEAD_DIM,
+                            dtype=torch.bfloat16, device=self.device)
+        for l in range(self.cfg.num_layers):
+            for kv in range(2):
+                K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv])
+        host = torch.empty(stage.shape, dtype=torch.bfloat16, pin_memory=True)
+        host.copy_(stage, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        self._swapped[request_id] = host
+
+    def swap_in(self, request_id: int, block_ids: list[int], tokens: int) -> None:
+        host = self._swapped.pop(request_id, None)
+        if host is None:
+            if tokens > 0:
+                raise EngineFault(f"request {request_id} readmitted without swapped KV")
+            return
+        n = host.shape[2]
+        if len(block_ids) < n:
+            raise EngineFault("readmission allocated fewer blocks than were swapped out")
+        ids = torch.tensor(block_ids[:n], dtype=torch.int32, device=self.device)
+        stage = host.to(self.device, non_blocking=True)
+        for l in range(self.cfg.num_layers):
+            for kv in range(2):
+                K.kv_swap_in(stage[l, kv], ids, self.kv[l, kv])

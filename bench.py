@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""SLO-meeting tokens/s of AccelGen's mixed-batch forward on B200 (BASELINE.json metric).
+
+One "step" = one engine iteration: order the queue, plan a BatchPlan (AccelGen),
+allocate KV blocks, run the mixed prefill+decode forward of OPT-13B (random bf16 weights) on the
+GPU(s), emit tokens.  Workload = BASELINE config 2 (90% <=1k prompts, 10% 4k-16k, output 1-2048,
+TBT 0.1875 s x U(0.75,1.25), TTFT per 512-token bucket x U(0.5,1.5)); the arrival rate scales
+with the GPU count (weak scaling), TP over the GPUs.  The engine runs on the live wall clock,
+so every SLO decision and every met/missed deadline is real.
+
+  value  SLO-meeting tokens / sum of CUDA-event forward times of the K timed steps (metadata
+         already resident in HBM; the device-side number)
+  e2e    the same tokens / wall time of the K steps through the public API (scheduler, packing,
+         pinned H2D of every step's metadata, forward, D2H of the next-token ids)
+  SLO-meeting tokens: tokens of a forward whose token event met its deadline (TTFT for a final
+  chunk, TBT for a decode, JCT for offline) or, for a non-final chunk, whose TTFT deadline has
+  not passed yet.  iter_slo_attainment = met / all token events in the window.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SLO-meeting tokens/s (OPT-13B mixed trace)"
+UNIT = "tokens/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--rate", type=float, default=None, help="arrival rate per GPU (req/s)")
+    ap.add_argument("--ramp-s", type=float, default=6.0, help="untimed trace seconds before warmup")
+    ap.add_argument("--profile", default=None, help="ModelProfile JSON (default: profiles/opt13b_b200_tp{N}.json)")
+    ap.add_argument("--kv-gb", type=float, default=80.0, help="KV pool per GPU (GB)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi SM clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": d["hbm_gbs"], "tensor": d["bf16_tflops"], "tensor_sustained": d["bf16_tflops_sustained"],
+                "source": "MEASURED_PEAKS.json (measured)"}
+    return {"hbm": 6650.0, "tensor": 1590.0, "tensor_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def default_profile(tp: int):
+    from paper_2503_13737_b200 import cost_model as cm
+    p = ROOT / "profiles" / f"opt13b_b200_tp{tp}.json"
+    if p.exists():
+        return cm.load_profile(p), str(p.relative_to(ROOT))
+    # declared fallback until the profiler has written one: S_pf 2048, linear fit guess
+    return cm.ModelProfile(hidden_size=5120, num_layers=40, pivot_forward_size=2048, pivot_time_s=0.06 / tp,
+                           fixed_overhead_s=0.006 / tp, kvc_capacity_tokens=0), "declared-default"
+
+
+def build_workload(args, world: int):
+    from paper_2503_13737_b200 import configs
+    from paper_2503_13737_b200.cost_model import ModelProfile
+    prof, prof_src = (default_profile(world) if args.profile is None else
+                      (__import__("paper_2503_13737_b200.cost_model", fromlist=["x"]).load_profile(args.profile),
+                       args.profile))
+    rate = (args.rate if args.rate is not None else 12.0) * world
+    cfg = configs.config2(profile=prof, arrival_rate=rate, num_requests=4000)
+    return cfg, prof, prof_src, rate
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2503_13737_b200 import tp as TP
+    from paper_2503_13737_b200 import workload
+    from paper_2503_13737_b200.cost_model import ModelProfile, forward_flops
+    from paper_2503_13737_b200.engine import Engine
+    from paper_2503_13737_b200.executor import CudaExecutor
+    from paper_2503_13737_b200.policies import PolicyConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        group = dist.group.WORLD
+    cfg, prof, prof_src, rate = build_workload(args, world)
+    mcfg = cfg.model
+    kv_tok_bytes = mcfg.kv_bytes_per_token(tp=world)
+    num_blocks = int(args.kv_gb * 1e9 // (32 * kv_tok_bytes))
+    prof = ModelProfile(**{**prof.__dict__, "kvc_capacity_tokens": num_blocks * 32})
+    uid = TP.share_nccl_id(rank, group) if world > 1 else None
+    s_pf = prof.pivot_forward_size
+    ex = CudaExecutor(mcfg, num_blocks, max_tokens=s_pf, max_seqs=2048,
+                      max_blocks_per_seq=(mcfg.pos_rows + 31) // 32, tp_rank=rank, tp_size=world, seed=0,
+                      init="opt", nccl_uid=uid)
+    torch.cuda.synchronize()
+
+    if rank != 0:
+        # followers: mirror rank 0's steps; report own device time for the max-over-ranks
+        ex.set_profiling(False)
+        dev = {"t": 0.0}
+        inner = ex.execute
+
+        def timed_exec(b):
+            r = inner(b)
+            dev["t"] += r.device_s
+            return r
+        ex.execute = timed_exec
+        TP.follower_loop(ex, group)
+        t = torch.tensor([dev["t"]], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        return
+
+    trace = workload.generate_trace(cfg.trace)
+    executor = TP.TPLeader(ex, group) if world > 1 else ex
+    eng = Engine(trace, prof, PolicyConfig(), executor, clock="wall", kv_blocks=num_blocks)
+
+    def next_step():
+        while not eng.done():
+            it = eng.step()
+            if it is not None:
+                return it
+        raise SystemExit("trace exhausted before the timed region ended; raise num_requests")
+
+    # untimed ramp to a loaded steady state, then W warm-up steps
+    while eng.clock < args.ramp_s:
+        next_step()
+    for _ in range(args.warmup):
+        next_step()
+
+    # ---------------- timed region: exactly K steps
+    batches = []
+    orig_exec = ex.execute
+
+    def recording_exec(b):
+        batches.append(b)
+        return orig_exec(b)
+    ex.execute = recording_exec
+    ex.set_profiling(True)
+    launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    recs = [next_step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    ex.execute = orig_exec
+    prof_k = ex.profile()
+    ex.set_profiling(False)
+    dev_s = sum(r.device_s for r in recs)
+    if world > 1:
+        executor.stop()
+        t = torch.tensor([dev_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+        dist.barrier()
+
+    slo_tokens = sum(r.slo_tokens for r in recs)
+    tokens = sum(r.forward_size for r in recs)
+    events = sum(r.events for r in recs)
+    met = sum(r.events_met for r in recs)
+    K = args.steps
+    # whole-forward tensor roofline: algorithmic FLOPs of every timed forward / device time
+    H, F, L, V = mcfg.hidden, mcfg.ffn, mcfg.num_layers, mcfg.vocab
+    flops = sum(forward_flops(b.seq_shapes(), len(b.logit_rows), H, F, L, V, world) for b in batches)
+    peaks = load_peaks()
+    gemm_cls = ("qkv_gemm", "out_gemm", "fc1_gemm", "fc2_gemm", "lmhead_gemm")
+    g_ms = sum(prof_k[c]["ms"] for c in gemm_cls)
+    g_fl = sum(prof_k[c]["flops"] for c in gemm_cls)
+    g_n = sum(prof_k[c]["launches"] for c in gemm_cls)
+    achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+    prof_total_ms = sum(v["ms"] for v in prof_k.values())
+    shares = {k: round(v["ms"] / prof_total_ms, 4) for k, v in prof_k.items() if prof_total_ms > 0 and v["ms"] > 0}
+    attn = prof_k["attention"]
+    line = {
+        "metric": METRIC,
+        "value": slo_tokens / dev_s if dev_s > 0 else 0.0,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": dev_s / K * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (BASELINE config-2 trace generator, random-init OPT-13B-shaped bf16 weights)",
+        "config": {"workload": "config2: OPT-13B mixed trace (90% <=1k, 10% 4k-16k prompts), AccelGen policy",
+                   "model": mcfg.name, "parallelism": f"tp{world}", "arrival_rate_rps": rate,
+                   "profile": prof_src, "pivot_forward_size": s_pf, "kv_pool_tokens": num_blocks * 32,
+                   "forward_tokens_per_step": tokens / K, "l2": "inputs larger than L2 (26 GB weights/step)",
+                   "clock": "wall (live)"},
+        "iter_slo_attainment": met / events if events else None,
+        "token_events": events,
+        "forward_tokens_per_s": tokens / dev_s if dev_s > 0 else 0.0,
+        "e2e": {"value": slo_tokens / wall if wall > 0 else 0.0, "unit": UNIT,
+                "h2d_bytes_per_step": (ex.h2d_bytes - h2d0) / K, "d2h_bytes_per_step": (ex.d2h_bytes - d2h0) / K},
+        "gpu_launches": ex.launches - launches0,
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (QKV/out/FC1/FC2/LM head)",
+                     "achieved": achieved, "peak": peaks["tensor_sustained"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["tensor_sustained"] if achieved else None,
+                     "peak_source": peaks["source"] + " bf16 sustained", "traffic": None,
+                     "launches": g_n, "per_launch_ms": g_ms / g_n if g_n else None,
+                     "per_launch_flops": g_fl / g_n if g_n else None},
+        "forward_roofline": {"achieved_tflops": flops / dev_s / 1e12 if dev_s else 0.0,
+                             "frac_of_sustained": flops / dev_s / 1e12 / peaks["tensor_sustained"] if dev_s else None},
+        "attention": {"ms": attn["ms"], "tflops": attn["flops"] / (attn["ms"] / 1e3) / 1e12 if attn["ms"] else 0.0,
+                      "gbs": attn["bytes"] / (attn["ms"] / 1e3) / 1e9 if attn["ms"] else 0.0},
+        "kernel_share": shares,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(mcfg, batches, world)
+    print(json.dumps(line), flush=True)
+
+
+def _median_batch(batches):
+    return sorted(batches, key=lambda b: b.num_tokens)[len(batches) // 2]
+
+
+def cpu_baseline(mcfg, batches, world, budget_s: float = 20.0) -> dict:
+    """The CPU oracle (the reference's path restated; oracle/) on a bounded sample: one OPT-13B
+    layer on the median timed batch, scaled to L layers + LM head."""
+    from oracle.bench_cpu import time_forward_sample
+    b = _median_batch(batches)
+    r = time_forward_sample(mcfg, b, budget_s=budget_s)
+    return {"value": r["tokens_per_s"], "unit": "tokens/s (forward; upper bound of SLO-meeting tokens/s)",
+            "cores": r["threads"], "kind": "port",
+            "sample": f"1 of {mcfg.num_layers} OPT-13B layers on the median timed batch (S_f={b.num_tokens}, "
+                      f"{len(b.cu_q) - 1} seqs), x{mcfg.num_layers} + LM head; {r['seconds']:.1f}s of CPU"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference's CPU implementation of the path (oracle port) on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.bench_cpu import reference_arm
+    cfg, prof, prof_src, rate = build_workload(args, world)
+    res = reference_arm(cfg, prof, steps=args.steps, warmup=args.warmup)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (same trace generator and shapes)",
+        "config": {"workload": "config2: OPT-13B mixed trace, AccelGen policy (oracle restatement)",
+                   "model": cfg.model.name, "parallelism": "cpu", "arrival_rate_rps": rate, "profile": prof_src},
+        "impl": "reference",
+        "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["threads"], "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

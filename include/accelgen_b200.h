@@ -42,6 +42,21 @@ extern "C" {
 
 typedef struct ag_model ag_model; /* opaque */
 
+/* Kernel classes of one forward, for ag_model_get_profile. */
+enum {
+  AG_K_EMBED = 0,
+  AG_K_LAYERNORM,
+  AG_K_QKV_GEMM,
+  AG_K_ATTENTION,
+  AG_K_OUT_GEMM,
+  AG_K_FC1_GEMM,
+  AG_K_FC2_GEMM,
+  AG_K_LMHEAD_GEMM,
+  AG_K_ARGMAX,
+  AG_K_ALLREDUCE,
+  AG_PROF_CLASSES
+};
+
 /* Model shape and capacities.  Mirrors the reference ModelProfile's shape fields
  * (cost_model.py:66-76: hidden_size, num_layers, bytes_per_element) plus the OPT architecture
  * constants the cost model folds away. */
@@ -117,6 +132,15 @@ AG_API int32_t ag_model_forward(ag_model* m, const ag_step* step, int32_t* out_t
  * ag_model_stage_step (used to time the kernels with inputs resident in HBM). */
 AG_API int32_t ag_model_stage_step(ag_model* m, const ag_step* step, void* stream);
 AG_API int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* logits_out, void* stream);
+
+/* Per-kernel-class CUDA-event profiling of ag_model_forward (on = 1 resets the counters).
+ * get_profile fills up to n entries per class: summed ms, algorithmic FLOPs and HBM bytes, launches. */
+AG_API int32_t ag_model_set_profiling(ag_model* m, int32_t on);
+AG_API int32_t ag_model_get_profile(ag_model* m, double* ms, double* flops, double* bytes, int64_t* counts, int32_t n);
+/* Kernel launches issued by the last forward (ours only; NCCL calls counted as AG_K_ALLREDUCE). */
+AG_API int64_t ag_model_last_launches(ag_model* m);
+/* Bytes of packed metadata (BatchPlan arrays + attention work list) copied H2D by the last step. */
+AG_API int64_t ag_model_last_h2d_bytes(ag_model* m);
 
 /* ---- individual kernels (device pointers), for parity tests and the profiler ---- */
 /* D[M,N] = A[M,K] . W[N,K]^T (+bias[N]) (+residual[M,ldr]) (ReLU); bf16 out unless out_f32. */

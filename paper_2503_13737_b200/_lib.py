@@ -15,6 +15,10 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libaccelgen_b200.so"
 
 AG_OK, AG_EINVAL, AG_ECUDA, AG_EALLOC, AG_EFAULT, AG_ENCCL = range(6)
 
+# kernel classes of ag_model_get_profile (include/accelgen_b200.h AG_K_*)
+PROF_CLASSES = ("embed", "layernorm", "qkv_gemm", "attention", "out_gemm", "fc1_gemm", "fc2_gemm", "lmhead_gemm",
+                "argmax", "allreduce")
+
 i32 = C.c_int32
 i64 = C.c_int64
 f32 = C.c_float
@@ -55,6 +59,10 @@ _SIGS = {
     "ag_model_forward": (i32, [vp, C.POINTER(Step), vp, vp, P_f32, vp]),
     "ag_model_stage_step": (i32, [vp, C.POINTER(Step), vp]),
     "ag_model_forward_staged": (i32, [vp, vp, vp, vp]),
+    "ag_model_set_profiling": (i32, [vp, i32]),
+    "ag_model_get_profile": (i32, [vp, vp, vp, vp, vp, i32]),
+    "ag_model_last_launches": (i64, [vp]),
+    "ag_model_last_h2d_bytes": (i64, [vp]),
     "ag_gemm_bf16": (i32, [vp, i32, vp, i32, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, vp]),
     "ag_kv_append": (i32, [vp, vp, i32, vp, i32, i32, i32, vp, vp, vp]),
     "ag_paged_attention": (i32, [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, vp, i32, vp, i64, vp]),

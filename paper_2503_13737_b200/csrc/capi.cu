@@ -179,6 +179,23 @@ struct ag_model {
   AttnWork work;
   ncclComm_t comm = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // per-kernel-class profiling (CUDA events around every launch of one forward)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_events;
+  struct ProfRec {
+    int cls;
+    int ev;
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof_pending;
+  double prof_ms[AG_PROF_CLASSES] = {};
+  double prof_flops[AG_PROF_CLASSES] = {};
+  double prof_bytes[AG_PROF_CLASSES] = {};
+  int64_t prof_count[AG_PROF_CLASSES] = {};
+  int64_t launches_last = 0;
+  int64_t h2d_last = 0;
+  int64_t launches_total = 0;
+  double attn_flops_step = 0.0, attn_bytes_step = 0.0;
 };
 
 namespace {
@@ -222,6 +239,46 @@ int32_t check_nccl(ncclResult_t r, const char* what) {
 int32_t allreduce_bf16(ag_model* m, bf16* buf, size_t count, cudaStream_t s) {
   if (m->cfg.tp_size == 1) return AG_OK;
   return check_nccl(nccl().AllReduce(buf, buf, count, ncclBfloat16, ncclSum, m->comm, s), "ncclAllReduce");
+}
+
+// Event bracket around one launch of kernel class `cls` (algorithmic flops / bytes attached).
+struct ProfScope {
+  ag_model* m;
+  int cls;
+  cudaStream_t s;
+  double flops, bytes;
+  int ev = -1;
+  ProfScope(ag_model* m_, int cls_, cudaStream_t s_, double f, double b) : m(m_), cls(cls_), s(s_), flops(f), bytes(b) {
+    m->launches_last += 1;
+    if (!m->prof_on) return;
+    const size_t need = m->prof_pending.size() * 2 + 2;
+    if (need > m->prof_events.size()) return;  // out of events: skip (counts stay exact)
+    ev = static_cast<int>(m->prof_pending.size() * 2);
+    cudaEventRecord(m->prof_events[ev], s);
+  }
+  ~ProfScope() {
+    if (ev < 0) return;
+    cudaEventRecord(m->prof_events[ev + 1], s);
+    m->prof_pending.push_back({cls, ev, flops, bytes});
+  }
+};
+
+void prof_harvest(ag_model* m) {
+  for (const auto& r : m->prof_pending) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, m->prof_events[r.ev], m->prof_events[r.ev + 1]) == cudaSuccess) {
+      m->prof_ms[r.cls] += ms;
+      m->prof_flops[r.cls] += r.flops;
+      m->prof_bytes[r.cls] += r.bytes;
+      m->prof_count[r.cls] += 1;
+    }
+  }
+  m->prof_pending.clear();
+}
+
+double gemm_flops(int M, int N, int K) { return 2.0 * M * static_cast<double>(N) * K; }
+double gemm_bytes(int M, int N, int K, int out_bytes) {
+  return 2.0 * (static_cast<double>(M) * K + static_cast<double>(N) * K) + static_cast<double>(out_bytes) * M * N;
 }
 
 }  // namespace
@@ -413,6 +470,17 @@ int32_t ag_model_stage_step(ag_model* m, const ag_step* st, void* stream) {
     if (st->logit_rows[i] < 0 || st->logit_rows[i] >= S) return fail(AG_EINVAL, "logit row out of range");
 
   build_attention_work(st->cu_q, st->ctx_len, B, m->heads_l, m->part_cap, m->work);
+  {
+    // exact causal attention work: q_i new rows over p_i cached + causal triangle
+    double fl = 0.0, by = 0.0;
+    for (int b = 0; b < B; ++b) {
+      const double q = st->cu_q[b + 1] - st->cu_q[b], p = st->ctx_len[b];
+      fl += 4.0 * m->hq * (q * p + q * (q + 1) / 2.0);
+      by += 2.0 * 2.0 * m->hq * (p + q) + 2.0 * 2.0 * m->hq * q;  // K+V read, q read + out write
+    }
+    m->attn_flops_step = fl;
+    m->attn_bytes_step = by;
+  }
   // pack
   uint8_t* h = m->meta_host;
   size_t off = 0;
@@ -436,6 +504,7 @@ int32_t ag_model_stage_step(ag_model* m, const ag_step* st, void* stream) {
   const size_t o_comb = put(m->work.combines.data(), sizeof(AttnCombine) * m->work.combines.size());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   AG_CUDA(cudaMemcpyAsync(m->meta_dev, m->meta_host, off, cudaMemcpyHostToDevice, s));
+  m->h2d_last = static_cast<int64_t>(off);
   const uint8_t* d = m->meta_dev;
   m->d_ids = reinterpret_cast<const int32_t*>(d + o_ids);
   m->d_pos = reinterpret_cast<const int32_t*>(d + o_pos);
@@ -461,123 +530,198 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
   const ag_model_config& c = m->cfg;
   const int S = m->S, H = c.hidden;
   const bool tp = c.tp_size > 1;
+  const double bf = 2.0;
+  m->launches_last = 0;
+  const double ln_bytes = bf * 2.0 * S * H;
   if (S > 0) {
-    AG_CUDA(ag::launch_embed(m->d_ids, m->d_pos, m->tok_emb, m->pos_emb, 2, S, H, c.vocab, c.pos_rows, m->resid, s));
+    {
+      ProfScope ps(m, AG_K_EMBED, s, 0.0, bf * 3.0 * S * H);
+      AG_CUDA(ag::launch_embed(m->d_ids, m->d_pos, m->tok_emb, m->pos_emb, 2, S, H, c.vocab, c.pos_rows, m->resid, s));
+    }
     const float qscale = 1.0f / std::sqrt(static_cast<float>(m->head_dim));
     for (int l = 0; l < c.num_layers; ++l) {
       const LayerState& L = m->layers[l];
       const ag_layer_weights& w = L.w;
-      // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
-      if (tp && l > 0) {
-        AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(m->layers[l - 1].w.fc2_b), nullptr,
-                                     static_cast<const bf16*>(w.ln1_g), static_cast<const bf16*>(w.ln1_b), c.ln_eps, S,
-                                     H, m->xln, s));
-      } else {
-        AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln1_g),
-                                     static_cast<const bf16*>(w.ln1_b), c.ln_eps, S, H, m->xln, s));
+      {
+        // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
+        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, (tp && l > 0) ? 2.0 * ln_bytes : ln_bytes);
+        if (tp && l > 0) {
+          AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(m->layers[l - 1].w.fc2_b), nullptr,
+                                       static_cast<const bf16*>(w.ln1_g), static_cast<const bf16*>(w.ln1_b), c.ln_eps,
+                                       S, H, m->xln, s));
+        } else {
+          AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln1_g),
+                                       static_cast<const bf16*>(w.ln1_b), c.ln_eps, S, H, m->xln, s));
+        }
       }
-      // QKV projection: q -> qbuf (scaled), K/V -> paged cache slots
-      ag::GemmEpilogue ep;
-      ep.mode = ag::kEpiQkv;
-      ep.bias = static_cast<const bf16*>(w.qkv_b);
-      ep.out = m->qbuf;
-      ep.ldc = m->hq;
-      ep.hq = m->hq;
-      ep.q_scale = qscale;
-      ep.kcache = L.kpool;
-      ep.vcache = L.vpool;
-      ep.slot_mapping = m->d_slot;
-      ep.heads = m->heads_l;
-      ep.head_dim = m->head_dim;
-      ep.block_size = c.block_size;
-      AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s));
-      // mixed paged attention
-      ag::AttnParams ap;
-      ap.q = m->qbuf;
-      ap.ldq = m->hq;
-      ap.kcache = L.kpool;
-      ap.vcache = L.vpool;
-      ap.block_table = m->d_bt;
-      ap.bt_stride = m->bt_stride;
-      ap.cu_q = m->d_cuq;
-      ap.ctx_len = m->d_ctx;
-      ap.out = m->attn;
-      ap.ldo = m->hq;
-      ap.part_o = m->part_o;
-      ap.part_ml = m->part_ml;
-      ap.heads = m->heads_l;
-      ap.block_size = c.block_size;
-      AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_items, m->d_comb, m->n_comb, s));
-      // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
-      ag::GemmEpilogue eo;
-      eo.ldc = H;
-      if (!tp) {
-        eo.bias = static_cast<const bf16*>(w.out_b);
-        eo.residual = m->resid;
-        eo.ldr = H;
-        eo.out = m->resid;
-      } else {
-        eo.out = m->proj;
+      {
+        // QKV projection: q -> qbuf (scaled), K/V -> paged cache slots (fused KV append)
+        ag::GemmEpilogue ep;
+        ep.mode = ag::kEpiQkv;
+        ep.bias = static_cast<const bf16*>(w.qkv_b);
+        ep.out = m->qbuf;
+        ep.ldc = m->hq;
+        ep.hq = m->hq;
+        ep.q_scale = qscale;
+        ep.kcache = L.kpool;
+        ep.vcache = L.vpool;
+        ep.slot_mapping = m->d_slot;
+        ep.heads = m->heads_l;
+        ep.head_dim = m->head_dim;
+        ep.block_size = c.block_size;
+        ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s));
       }
-      AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s));
+      {
+        ag::AttnParams ap;
+        ap.q = m->qbuf;
+        ap.ldq = m->hq;
+        ap.kcache = L.kpool;
+        ap.vcache = L.vpool;
+        ap.block_table = m->d_bt;
+        ap.bt_stride = m->bt_stride;
+        ap.cu_q = m->d_cuq;
+        ap.ctx_len = m->d_ctx;
+        ap.out = m->attn;
+        ap.ldo = m->hq;
+        ap.part_o = m->part_o;
+        ap.part_ml = m->part_ml;
+        ap.heads = m->heads_l;
+        ap.block_size = c.block_size;
+        ProfScope ps(m, AG_K_ATTENTION, s, m->attn_flops_step, m->attn_bytes_step);
+        if (m->n_comb > 0) m->launches_last += 1;
+        AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_items, m->d_comb, m->n_comb, s));
+      }
+      {
+        // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
+        ag::GemmEpilogue eo;
+        eo.ldc = H;
+        if (!tp) {
+          eo.bias = static_cast<const bf16*>(w.out_b);
+          eo.residual = m->resid;
+          eo.ldr = H;
+          eo.out = m->resid;
+        } else {
+          eo.out = m->proj;
+        }
+        ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
+        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s));
+      }
       if (tp) {
-        AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+        {
+          ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
+          AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+        }
+        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, 2.0 * ln_bytes);
         AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(w.out_b), nullptr,
                                      static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps, S,
                                      H, m->xln, s));
       } else {
+        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ln_bytes);
         AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln2_g),
                                      static_cast<const bf16*>(w.ln2_b), c.ln_eps, S, H, m->xln, s));
       }
-      // FC1 + bias + ReLU
-      ag::GemmEpilogue e1;
-      e1.bias = static_cast<const bf16*>(w.fc1_b);
-      e1.relu = 1;
-      e1.out = m->ffn;
-      e1.ldc = m->ffn_l;
-      AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s));
-      // FC2 (+bias +residual / partial + all-reduce)
-      ag::GemmEpilogue e2;
-      e2.ldc = H;
-      if (!tp) {
-        e2.bias = static_cast<const bf16*>(w.fc2_b);
-        e2.residual = m->resid;
-        e2.ldr = H;
-        e2.out = m->resid;
-      } else {
-        e2.out = m->proj;
+      {
+        ag::GemmEpilogue e1;
+        e1.bias = static_cast<const bf16*>(w.fc1_b);
+        e1.relu = 1;
+        e1.out = m->ffn;
+        e1.ldc = m->ffn_l;
+        ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s));
       }
-      AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s));
-      if (tp) AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+      {
+        ag::GemmEpilogue e2;
+        e2.ldc = H;
+        if (!tp) {
+          e2.bias = static_cast<const bf16*>(w.fc2_b);
+          e2.residual = m->resid;
+          e2.ldr = H;
+          e2.out = m->resid;
+        } else {
+          e2.out = m->proj;
+        }
+        ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
+        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s));
+      }
+      if (tp) {
+        ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
+        AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
+      }
     }
     if (tp) {  // fold the last FC2 all-reduce into the residual stream
       const ag_layer_weights& wl = m->layers[c.num_layers - 1].w;
+      ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, 2.0 * ln_bytes);
       AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(wl.fc2_b), nullptr, m->final_g,
                                    m->final_b, c.ln_eps, S, H, m->xln, s));
     }
   }
   const int NL = m->n_logit;
   if (NL > 0) {
-    // final LayerNorm only on the rows that emit a token (logit skip)
-    AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H,
-                                 m->lm_in, s));
+    {
+      // final LayerNorm only on the rows that emit a token (logit skip)
+      ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, bf * 2.0 * NL * H);
+      AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H,
+                                   m->lm_in, s));
+    }
     ag::GemmEpilogue el;
     el.out = logits_out ? static_cast<void*>(logits_out) : static_cast<void*>(m->logits);
     el.ldc = m->vocab_l;
     el.out_f32 = 1;
     float* lg = static_cast<float*>(el.out);
-    AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s));
+    {
+      ProfScope ps(m, AG_K_LMHEAD_GEMM, s, gemm_flops(NL, m->vocab_l, H), gemm_bytes(NL, m->vocab_l, H, 4));
+      AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s));
+    }
     if (!tp) {
+      ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 4.0 * NL * m->vocab_l);
       AG_CUDA(ag::launch_argmax(lg, NL, m->vocab_l, m->vocab_l, 0, nullptr, out_tokens_dev, s));
     } else {
-      AG_CUDA(ag::launch_argmax(lg, NL, m->vocab_l, m->vocab_l, m->vocab_off, m->cand_val, m->cand_idx, s));
-      AG_TRY(check_nccl(nccl().AllGather(m->cand_val, m->gathered_val, NL, ncclFloat32, m->comm, s), "allgather"));
-      AG_TRY(check_nccl(nccl().AllGather(m->cand_idx, m->gathered_idx, NL, ncclInt32, m->comm, s), "allgather"));
+      {
+        ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 4.0 * NL * m->vocab_l);
+        AG_CUDA(ag::launch_argmax(lg, NL, m->vocab_l, m->vocab_l, m->vocab_off, m->cand_val, m->cand_idx, s));
+      }
+      {
+        ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, 8.0 * NL * c.tp_size);
+        AG_TRY(check_nccl(nccl().AllGather(m->cand_val, m->gathered_val, NL, ncclFloat32, m->comm, s), "allgather"));
+        AG_TRY(check_nccl(nccl().AllGather(m->cand_idx, m->gathered_idx, NL, ncclInt32, m->comm, s), "allgather"));
+      }
+      ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 8.0 * NL * c.tp_size);
       AG_CUDA(ag::launch_argmax_merge(m->gathered_val, m->gathered_idx, c.tp_size, NL, out_tokens_dev, s));
     }
   }
+  m->launches_total += m->launches_last;
   return AG_OK;
 }
+
+int32_t ag_model_set_profiling(ag_model* m, int32_t on) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  m->prof_on = on != 0;
+  m->prof_pending.clear();
+  for (int i = 0; i < AG_PROF_CLASSES; ++i) {
+    m->prof_ms[i] = m->prof_flops[i] = m->prof_bytes[i] = 0.0;
+    m->prof_count[i] = 0;
+  }
+  if (m->prof_on && m->prof_events.empty()) {
+    m->prof_events.resize(2 * (16 * static_cast<size_t>(m->cfg.num_layers) + 64));
+    for (auto& e : m->prof_events) AG_CUDA(cudaEventCreate(&e));
+  }
+  return AG_OK;
+}
+
+int32_t ag_model_get_profile(ag_model* m, double* ms, double* flops, double* bytes, int64_t* counts, int32_t n) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  for (int i = 0; i < std::min<int>(n, AG_PROF_CLASSES); ++i) {
+    if (ms) ms[i] = m->prof_ms[i];
+    if (flops) flops[i] = m->prof_flops[i];
+    if (bytes) bytes[i] = m->prof_bytes[i];
+    if (counts) counts[i] = m->prof_count[i];
+  }
+  return AG_OK;
+}
+
+int64_t ag_model_last_launches(ag_model* m) { return m ? m->launches_last : -1; }
+int64_t ag_model_last_h2d_bytes(ag_model* m) { return m ? m->h2d_last : -1; }
 
 int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, float* logits_out, float* device_ms,
                          void* stream) {
@@ -591,6 +735,7 @@ int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, fl
     AG_CUDA(cudaMemcpyAsync(m->tok_host, m->out_tok, sizeof(int32_t) * m->n_logit, cudaMemcpyDeviceToHost, s));
   AG_CUDA(cudaStreamSynchronize(s));
   if (device_ms) AG_CUDA(cudaEventElapsedTime(device_ms, m->ev0, m->ev1));
+  if (m->prof_on) prof_harvest(m);
   if (out_tokens && m->n_logit > 0) std::memcpy(out_tokens, m->tok_host, sizeof(int32_t) * m->n_logit);
   return AG_OK;
 }

@@ -299,6 +299,7 @@ class Engine:
 
     # -------------------------------------------------------------- one iteration
     def step(self) -> IterationRecord | None:
+        t_step0 = time.perf_counter()
         self._admit()
         if not self.queue:
             if self._next_arrival < len(self.trace):
@@ -391,7 +392,7 @@ class Engine:
         elif self.clock_mode == "device":
             elapsed = res.elapsed_s
         else:
-            elapsed = wall
+            elapsed = time.perf_counter() - t_step0  # scheduling + packing + H2D + forward + D2H
         elapsed += swap_tokens * self.swap_cost
         self.clock = start + elapsed
         now = self.clock

@@ -77,7 +77,20 @@ class CudaExecutor:
         self.logits_buf = torch.empty(max_seqs, cfg.vocab // tp_size, dtype=torch.float32, device=self.device) \
             if parity_logits else None
         self.steps = 0
-        self.launches_per_step = None
+        self.launches = 0       # our kernel launches summed over executed steps
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def set_profiling(self, on: bool) -> None:
+        _lib.check(self.lib.ag_model_set_profiling(self.handle, int(on)))
+
+    def profile(self) -> dict:
+        n = len(_lib.PROF_CLASSES)
+        ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        _lib.check(self.lib.ag_model_get_profile(self.handle, ms, fl, by, cnt, n))
+        return {name: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
+                for i, name in enumerate(_lib.PROF_CLASSES)}
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -127,6 +140,9 @@ class CudaExecutor:
         wall = time.perf_counter() - t0
         del keep
         self.steps += 1
+        self.launches += int(self.lib.ag_model_last_launches(self.handle))
+        self.h2d_bytes += int(self.lib.ag_model_last_h2d_bytes(self.handle))
+        self.d2h_bytes += 4 * n
         logits = self.logits_buf[:n].cpu() if self.logits_buf is not None else None
         dev_s = self._dev_ms.value / 1e3
         return StepResult(token_ids=out[:n].copy(), elapsed_s=dev_s, device_s=dev_s, wall_s=wall, logits=logits)

@@ -50,42 +50,49 @@ def test_config1_trace_parity():
     assert agree >= TOKEN_AGREEMENT
 
 
+def _make_batch(pool, cfg, segs):
+    from paper_2503_13737_b200.engine import DeviceBatch, synthetic_tokens
+    ids, pos, slot, cu, ctx, tabs, lrows, rids = [], [], [], [0], [], [], [], []
+    for rid, start, n in segs:
+        d = pool.demand_prompt_chunk(rid, n) if (n > 1 or not pool.is_resident(rid)) else pool.demand_tg(rid)
+        pool.allocate(rid, d)
+        p = np.arange(start, start + n, dtype=np.int32)
+        ids.append(synthetic_tokens(rid, p, cfg.vocab)); pos.append(p)
+        slot.append(np.asarray(pool.slots(rid, start, n), np.int32)); ctx.append(start)
+        cu.append(cu[-1] + n); tabs.append(pool.block_table(rid)); lrows.append(cu[-1] - 1); rids.append(rid)
+    bt = np.zeros((len(tabs), max(map(len, tabs))), np.int32)
+    for i, t in enumerate(tabs):
+        bt[i, :len(t)] = t
+    return DeviceBatch(rids, np.concatenate(ids), np.concatenate(pos), np.asarray(cu, np.int32),
+                       np.asarray(ctx, np.int32), bt, np.concatenate(slot), np.asarray(lrows, np.int32), rids)
+
+
 def test_13b_shape_mixed_batch_two_layers():
     """OPT-13B layer shapes (H=5120, 40 heads, FFN 20480), 2 layers, one mixed batch:
     a 1500-token chunk on a 3000-token prefix + a fresh 300-token prompt + 40 decodes."""
     from paper_2503_13737_b200.executor import CudaExecutor
     from paper_2503_13737_b200.kvc import BlockPool
-    from paper_2503_13737_b200.engine import DeviceBatch, synthetic_tokens
     cfg = M.OPTConfig("opt-13b-2l", hidden=5120, num_layers=2, num_heads=40, ffn=20480, max_positions=8192)
     w = M.init_weights(cfg, seed=1, init="test")
     pool = BlockPool(4096)
     dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=4096, max_seqs=128, weights=w, parity_logits=True)
     ref = OracleExecutor(cfg, w, pool.total_blocks)
-    # prefill the prefixes through both executors, then run the mixed step
-    seqs = [(0, 3000, 1500), (1, 0, 300)] + [(2 + i, 100 + 37 * i, 1) for i in range(40)]
-    for phase in (0, 1):
-        ids, pos, slot, cu, ctx, tabs, lrows = [], [], [], [0], [], [], []
-        rids = []
-        for rid, prefix, q in seqs:
-            if phase == 0:
-                if prefix == 0:
-                    continue
-                start, n = 0, prefix
-            else:
-                start, n = prefix, q
-            from paper_2503_13737_b200.kvc import KvcDemand
-            dmd = pool.demand_prompt_chunk(rid, n)
-            pool.allocate(rid, dmd)
-            p = np.arange(start, start + n, dtype=np.int32)
-            ids.append(synthetic_tokens(rid, p, cfg.vocab)); pos.append(p)
-            slot.append(np.asarray(pool.slots(rid, start, n), np.int32)); ctx.append(start)
-            cu.append(cu[-1] + n); tabs.append(pool.block_table(rid)); lrows.append(cu[-1] - 1); rids.append(rid)
-        bt = np.zeros((len(tabs), max(map(len, tabs))), np.int32)
-        for i, t in enumerate(tabs):
-            bt[i, :len(t)] = t
-        b = DeviceBatch(rids, np.concatenate(ids), np.concatenate(pos), np.asarray(cu, np.int32),
-                        np.asarray(ctx, np.int32), bt, np.concatenate(slot), np.asarray(lrows, np.int32), rids)
-        a, r = dev.execute(b), ref.execute(b)
+    decodes = [(2 + i, 50 + 13 * i) for i in range(40)]
+    # prefixes, <= 4096 tokens per forward
+    prefill = [(0, 0, 3000)] + [(rid, 0, p) for rid, p in decodes]
+    batch, used = [], 0
+    for seg in prefill:
+        if used + seg[2] > 4000:
+            b = _make_batch(pool, cfg, batch)
+            dev.execute(b); ref.execute(b)
+            batch, used = [], 0
+        batch.append(seg)
+        used += seg[2]
+    b = _make_batch(pool, cfg, batch)
+    dev.execute(b); ref.execute(b)
+    mixed = [(0, 3000, 1500), (1, 0, 300)] + [(rid, p, 1) for rid, p in decodes]
+    b = _make_batch(pool, cfg, mixed)
+    a, r = dev.execute(b), ref.execute(b)
     n = len(b.logit_rows)
     d = (a.logits[:n] - r.logits[:n]).abs().max().item()
     agree = float((a.token_ids == r.token_ids).mean())

@@ -1,0 +1,52 @@
+"""Scheduler decisions of the product (policies.py + engine.py) vs the brute-force oracle
+restatement (oracle/sched.py): chunk sizes, batch composition, preemptions and physical KV block
+tables must be identical step for step under the virtual clock (north_star: bit-exact)."""
+import pytest
+
+from oracle.sched import OracleScheduler
+from paper_2503_13737_b200 import configs, cost_model as cm, workload as wl
+from paper_2503_13737_b200.engine import Engine
+from paper_2503_13737_b200.policies import PolicyConfig
+
+
+def _compare(trace, prof, kv_blocks=None, max_steps=None):
+    eng = Engine(trace, prof, PolicyConfig(), kv_blocks=kv_blocks, check_invariants=True)
+    eng.keep_history = True
+    eng.run(max_steps=max_steps)
+    orc = OracleScheduler(trace, prof, kv_blocks=kv_blocks)
+    log = orc.run(max_steps=max_steps)
+    assert len(log) == len(eng.plans)
+    for i, (plan, tables, ref) in enumerate(zip(eng.plans, eng.tables, log)):
+        ours = [(s.request_id, s.chunk_len, s.is_final_chunk) for s in plan.selections]
+        assert ours == [(r, c, f) for r, c, f, _ in ref["sel"]], f"step {i}"
+        assert plan.token_budget == ref["s_b"], f"step {i}"
+        assert plan.preempted == ref["preempted"], f"step {i}"
+        assert {r: list(map(int, t)) for r, t in tables.items()} == ref["tables"], f"step {i}"
+    return len(log)
+
+
+def test_config1_decisions_match_oracle():
+    c = configs.config1()
+    n = _compare(wl.generate_trace(c.trace), c.trace.profile)
+    assert n > 1000
+
+
+def test_kv_pressure_with_preemption_matches_oracle():
+    """Small KV pool (paper-like capped regime): urgency, preemption (swap-out) and readmission."""
+    c = configs.config1()
+    prof = cm.ModelProfile(hidden_size=256, num_layers=2, pivot_forward_size=256, pivot_time_s=0.002,
+                           fixed_overhead_s=0.002, kvc_capacity_tokens=48 * 32)
+    trace = wl.generate_trace(wl.TraceConfig(**{**c.trace.__dict__, "num_requests": 40, "profile": prof,
+                                                "long_fraction": 0.0,
+                                                "output_len_dist": wl.LengthDist("uniform", 100, 400)}))
+    eng = Engine(trace, prof, PolicyConfig(), kv_blocks=48)
+    assert eng.run().preemptions > 20  # the scenario really exercises preemption
+    n = _compare(trace, prof, kv_blocks=48)
+    assert n > 1000
+
+
+def test_b200_like_profile_with_offline_matches_oracle():
+    prof = cm.ModelProfile(hidden_size=5120, num_layers=40, pivot_forward_size=2048, pivot_time_s=0.05,
+                           fixed_overhead_s=0.005, kvc_capacity_tokens=60000)
+    cfg = configs.config5(profile=prof, num_requests=120, arrival_rate=12.0).trace
+    _compare(wl.generate_trace(cfg), prof, max_steps=2000)

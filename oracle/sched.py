@@ -155,17 +155,19 @@ class OracleScheduler:
         new_here = set()
         B, deferred = [], []
         s_f = used = 0
+        tg_left = len([r for r in urgent if not self.prompt_left(r)])
         for r in urgent:
             if self.prompt_left(r):
                 if self.era_blocked(r, active):
                     deferred.append(r.rid)
                     continue
-                c = min(r.remaining, max(1, s_b - s_f))
+                c = min(r.remaining, max(1, s_b - s_f - tg_left))
                 if r.long and r.rid not in active:
                     active.add(r.rid)
                     new_here.add(r.rid)
             else:
                 c = 1
+                tg_left -= 1
             blk = pool.need(r, c)
             B.append([r, c, blk])
             s_f += c

@@ -38,9 +38,11 @@ CSV_COLUMNS = ("policy", "tokens_per_s", "reqs_per_s", "goodput", "slo_attainmen
 
 
 # ----------------------------------------------------------------------------- device batch
-def synthetic_tokens(request_id: int, positions: np.ndarray, vocab: int) -> np.ndarray:
-    """Deterministic token ids in [4, vocab) keyed by (request, position) (splitmix64)."""
-    x = (np.uint64(request_id) << np.uint64(32)) ^ positions.astype(np.uint64)
+def synthetic_tokens(request_id, positions: np.ndarray, vocab: int) -> np.ndarray:
+    """Deterministic token ids in [4, vocab) keyed by (request, position) (splitmix64);
+    request_id may be a scalar or an array aligned with positions."""
+    rid = np.asarray(request_id).astype(np.uint64)
+    x = (rid << np.uint64(32)) ^ positions.astype(np.uint64)
     with np.errstate(over="ignore"):
         x = x + np.uint64(0x9E3779B97F4A7C15)
         x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
@@ -334,10 +336,13 @@ class Engine:
             self.clock = min(nxt, self.clock + self.stats.t_max)
             return None
 
-        # ---- allocation + batch packing
+        # ---- allocation + batch packing (vectorised: one numpy pass over all tokens)
         free_before = self.pool.free_blocks
-        rows_tok, rows_pos, rows_slot, cu, ctx_len, tables, logit_rows, logit_ids = [], [], [], [0], [], [], [], []
-        for sel in plan.selections:
+        n_sel = len(plan.selections)
+        chunk = np.empty(n_sel, np.int64)
+        before_arr = np.empty(n_sel, np.int64)
+        tables: list[list[int]] = []
+        for i, sel in enumerate(plan.selections):
             e = by_id[sel.request_id]
             rid = sel.request_id
             try:
@@ -349,34 +354,37 @@ class Engine:
                     rec = self.metrics.requests[rid]
                     if rec.preempt_time is not None:
                         self.stats.observe_preemption_duration(start - rec.preempt_time)
-                prompt = has_prompt_left(e)
                 before = self.pool.tokens_stored(rid)
-                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if prompt else self.pool.demand_tg(rid))
+                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if has_prompt_left(e)
+                          else self.pool.demand_tg(rid))
                 self.pool.allocate(rid, demand)
             except (AllocationError, StateError) as exc:
                 raise EngineFault(f"plan infeasible against the pool: {exc}") from exc
-            pos = np.arange(before, before + sel.chunk_len, dtype=np.int32)
-            rows_pos.append(pos)
-            rows_tok.append(synthetic_tokens(rid, pos, self.executor.vocab))
-            rows_slot.append(np.asarray(self.pool.slots(rid, before, sel.chunk_len), dtype=np.int32))
-            ctx_len.append(before)
-            cu.append(cu[-1] + sel.chunk_len)
+            chunk[i] = sel.chunk_len
+            before_arr[i] = before
             tables.append(self.pool.block_table(rid))
-            if sel.is_final_chunk:
-                logit_rows.append(cu[-1] - 1)
-                logit_ids.append(rid)
         if free_before - self.pool.free_blocks != plan.blocks_needed:
             raise EngineFault(f"allocated {free_before - self.pool.free_blocks} blocks, plan expected "
                               f"{plan.blocks_needed}")
+        cu = np.zeros(n_sel + 1, np.int64)
+        np.cumsum(chunk, out=cu[1:])
+        S = int(cu[-1])
+        seq_of_tok = np.repeat(np.arange(n_sel), chunk)
+        positions = (np.arange(S) - cu[seq_of_tok] + before_arr[seq_of_tok]).astype(np.int32)
+        rids_arr = np.asarray([s.request_id for s in plan.selections], np.int64)
+        token_ids = synthetic_tokens(rids_arr[seq_of_tok], positions, self.executor.vocab)
         stride = max(len(t) for t in tables)
-        bt = np.zeros((len(tables), stride), dtype=np.int32)
+        bt = np.zeros((n_sel, stride), dtype=np.int32)
         for i, t in enumerate(tables):
             bt[i, :len(t)] = t
-        batch = DeviceBatch(request_ids=[s.request_id for s in plan.selections], token_ids=np.concatenate(rows_tok),
-                            positions=np.concatenate(rows_pos), cu_q=np.asarray(cu, dtype=np.int32),
-                            ctx_len=np.asarray(ctx_len, dtype=np.int32), block_table=bt,
-                            slot_mapping=np.concatenate(rows_slot), logit_rows=np.asarray(logit_rows, dtype=np.int32),
-                            logit_request_ids=logit_ids)
+        bs = self.pool.block_size
+        slots = (bt[seq_of_tok, positions // bs] * bs + positions % bs).astype(np.int32)
+        final = np.fromiter((s.is_final_chunk for s in plan.selections), bool, n_sel)
+        logit_rows = (cu[1:][final] - 1).astype(np.int32)
+        logit_ids = [int(r) for r in rids_arr[final]]
+        batch = DeviceBatch(request_ids=[s.request_id for s in plan.selections], token_ids=token_ids,
+                            positions=positions, cu_q=cu.astype(np.int32), ctx_len=before_arr.astype(np.int32),
+                            block_table=bt, slot_mapping=slots, logit_rows=logit_rows, logit_request_ids=logit_ids)
         if self.check:
             self.pool.check_conservation()
         if self.keep_history:

@@ -10,9 +10,10 @@ ambiguity pinned once (SURVEY §8c'):
 * Token budget S_b = max(1, min(floor(S_pf * slo_min / T_pf), cap)), cap defaults to S_pf
   (SPEC.md:384-392).  slo_min is the smallest ONLINE iteration SLO among the urgent entries and
   the head of the queue; with no online entry S_b = cap.
-* Algorithm 1: urgent entries join B in queue order; a pending prompt takes
-  min(remaining, max(1, S_b - S_f)) tokens (sequential token selection, PAPER §4.2), a TG or
-  preempted TG task 1 token.  While S_f > S_b or B's block demand exceeds the free blocks, the
+* Algorithm 1: urgent entries join B in queue order; a TG or preempted TG task takes 1 token, a
+  pending prompt takes min(remaining, max(1, S_b - S_f - R)) tokens where R counts the urgent
+  TG tasks not yet placed (sequential token selection, PAPER §4.2, with the returned decodes
+  "retained in the batch as much as possible", PAPER §4.4).  While S_f > S_b or B's block demand exceeds the free blocks, the
   member with max T_r (ties: later queue position) leaves B; if it holds blocks it is preempted
   (swapped out, freeing them), otherwise it is deferred.
 * Algorithm 2 (select_requests): window = non-urgent entries with T_r <= T_r^1 + gamma.  Every
@@ -237,17 +238,22 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
     members: list[list] = []  # [entry, chunk, blocks]
     s_f = used = 0
     deferred: list[int] = []
+    # every urgent TG / preempted-TG task needs exactly one token; reserve those before sizing the
+    # urgent prompt chunks so a chunk never crowds the returned decodes out of B (PAPER §4.4:
+    # "the previous TG requests should be retained in the batch as much as possible")
+    reserved = sum(1 for e in urgent if not has_prompt_left(e))
     for e in urgent:
         if has_prompt_left(e):
             if _era_blocked(e, cfg, long_active):
                 deferred.append(e.request_id)
                 continue
-            c = min(e.remaining_prompt_tokens, max(1, s_b - s_f))
+            c = min(e.remaining_prompt_tokens, max(1, s_b - s_f - reserved))
             if e.is_long and e.request_id not in long_active:
                 long_active.add(e.request_id)
                 started_here.add(e.request_id)
         else:
             c = 1
+            reserved -= 1
         blk = step_blocks(e, c, pool)
         members.append([e, c, blk])
         s_f += c
@@ -255,21 +261,30 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
 
     free = pool.free_blocks
     preempted: list[int] = []
-    while members and (s_f > s_b or used > free):
-        victim = max(members, key=lambda m: (t_r[m[0].request_id], position[m[0].request_id]))
-        members.remove(victim)
-        e, c, blk = victim
-        s_f -= c
-        used -= blk
-        rid = e.request_id
-        if pool.is_resident(rid):
-            preempted.append(rid)
-            free += pool.blocks_held(rid)
-        else:
-            deferred.append(rid)
-        if rid in started_here:
-            long_active.discard(rid)
-            started_here.discard(rid)
+    if members and (s_f > s_b or used > free):
+        # repeatedly drop the member with max T_r (ties: later queue position) until B fits:
+        # equivalent to walking the members in descending (T_r, position) order
+        order = sorted(range(len(members)),
+                       key=lambda i: (t_r[members[i][0].request_id], position[members[i][0].request_id]),
+                       reverse=True)
+        dropped = set()
+        for i in order:
+            if not (s_f > s_b or used > free):
+                break
+            e, c, blk = members[i]
+            dropped.add(i)
+            s_f -= c
+            used -= blk
+            rid = e.request_id
+            if pool.is_resident(rid):
+                preempted.append(rid)
+                free += pool.blocks_held(rid)
+            else:
+                deferred.append(rid)
+            if rid in started_here:
+                long_active.discard(rid)
+                started_here.discard(rid)
+        members = [m for i, m in enumerate(members) if i not in dropped]
 
     chosen = [(m[0], m[1], m[2]) for m in members]
     skip = {e.request_id for e in urgent} | set(preempted) | set(deferred)

@@ -1,0 +1,105 @@
+"""B200 profiler: measure the iteration-time cost model the chunker consumes.
+
+The paper finds the pivot forward size S_pf by sweeping the forward size until throughput
+saturates and records the batch time T_pf there (PAPER §4.2, "we measure the pivot forward size
+(S_pf) by varying the forward size ... and measure the corresponding batch execution time";
+the saturation criterion <3% marginal gain is in PAPER.md:726).  The reference's stand-in only
+derives it from a peak FLOP/s (cost_model.py:144-159).  Here the sweep runs the real mixed
+forward on the GPU (CUDA-event time of ag_model_forward), fits the reference's linear model
+T(S_f) = T_0 + T_pf * S_f / S_pf by least squares, and writes a ModelProfile JSON
+(PROFILE_KEYS, cost_model.py:23-31) that bench.py / the engine load with load_profile.
+
+  python -m paper_2503_13737_b200.profiler --out profiles/opt13b_b200_tp1.json
+"""
+from __future__ import annotations
+
+import argparse
+import json
+from pathlib import Path
+
+import numpy as np
+
+SWEEP = (64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192)
+
+
+def prefill_batch(pool, cfg, s_f: int, seq_len: int, rid0: int):
+    """S_f tokens of fresh prompts (seq_len each, the last one shorter)."""
+    from .engine import DeviceBatch, synthetic_tokens
+    ids, pos, slot, cu, ctx, tabs, lr, rids = [], [], [], [0], [], [], [], []
+    left, rid = s_f, rid0
+    while left > 0:
+        n = min(seq_len, left)
+        pool.allocate(rid, pool.demand_prompt_chunk(rid, n))
+        p = np.arange(0, n, dtype=np.int32)
+        ids.append(synthetic_tokens(rid, p, cfg.vocab)); pos.append(p)
+        slot.append(np.asarray(pool.slots(rid, 0, n), np.int32)); ctx.append(0)
+        cu.append(cu[-1] + n); tabs.append(pool.block_table(rid)); lr.append(cu[-1] - 1); rids.append(rid)
+        left -= n
+        rid += 1
+    bt = np.zeros((len(tabs), max(map(len, tabs))), np.int32)
+    for i, t in enumerate(tabs):
+        bt[i, :len(t)] = t
+    return DeviceBatch(rids, np.concatenate(ids), np.concatenate(pos), np.asarray(cu, np.int32),
+                       np.asarray(ctx, np.int32), bt, np.concatenate(slot), np.asarray(lr, np.int32), rids), rid
+
+
+def sweep(cfg, tp: int = 1, sizes=SWEEP, seq_len: int = 512, reps: int = 5, executor=None) -> list[dict]:
+    from .executor import CudaExecutor
+    from .kvc import BlockPool
+    max_t = max(sizes)
+    n_blocks = 2 * (max_t // 32 + len(sizes) * 4)
+    ex = executor or CudaExecutor(cfg, n_blocks, max_tokens=max_t, max_seqs=max_t // seq_len + 8, tp_size=tp)
+    out = []
+    rid = 0
+    for s_f in sizes:
+        times = []
+        for r in range(reps + 2):
+            pool = BlockPool(n_blocks)
+            b, rid = prefill_batch(pool, cfg, s_f, seq_len, rid)
+            res = ex.execute(b)
+            if r >= 2:
+                times.append(res.device_s)
+        t = float(np.median(times))
+        out.append({"s_f": s_f, "seconds": t, "tokens_per_s": s_f / t})
+    return out
+
+
+def fit(points: list[dict], hidden: int, num_layers: int, kvc_tokens: int, gain: float = 0.03) -> dict:
+    """Least-squares T = T_0 + a*S_f over the sweep; S_pf = smallest size whose throughput is within
+    `gain` of the best measured (the paper's <3% marginal-gain saturation rule)."""
+    s = np.array([p["s_f"] for p in points], float)
+    t = np.array([p["seconds"] for p in points], float)
+    thr = s / t
+    best = thr.max()
+    s_pf = int(s[np.argmax(thr >= (1.0 - gain) * best)])
+    big = s >= 256
+    a, t0 = np.polyfit(s[big], t[big], 1)
+    t0 = max(0.0, float(t0))
+    return {"hidden_size": hidden, "num_layers": num_layers, "pivot_forward_size": s_pf,
+            "pivot_time_s": float(a * s_pf), "bytes_per_element": 2, "fixed_overhead_s": t0,
+            "kvc_capacity_tokens": int(kvc_tokens)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="opt-13b")
+    ap.add_argument("--tp", type=int, default=1)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--kv-gb", type=float, default=80.0)
+    args = ap.parse_args()
+    from . import model as M
+    from .cost_model import ModelProfile, save_profile
+    cfg = M.PRESETS[args.model]()
+    pts = sweep(cfg, args.tp)
+    kv_tokens = int(args.kv_gb * 1e9 // (32 * cfg.kv_bytes_per_token(args.tp))) * 32
+    prof = fit(pts, cfg.hidden, cfg.num_layers, kv_tokens)
+    out = Path(args.out or f"profiles/opt13b_b200_tp{args.tp}.json")
+    out.parent.mkdir(parents=True, exist_ok=True)
+    save_profile(ModelProfile(**prof), out)
+    out.with_name(out.stem + "_sweep.json").write_text(json.dumps({"model": args.model, "tp": args.tp,
+                                                                    "points": pts, "fit": prof}, indent=1))
+    print(json.dumps({"profile": prof, "points": pts}))
+
+
+if __name__ == "__main__":
+    main()

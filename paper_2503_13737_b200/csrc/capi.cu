@@ -163,6 +163,8 @@ struct ag_model {
   int32_t* out_tok = nullptr;
   float *part_o = nullptr, *part_ml = nullptr;
   int part_cap = 0;
+  float* splitk_ws = nullptr;
+  int64_t splitk_cap = 0;
   // metadata: one pinned host buffer mirrored by one device buffer
   uint8_t* meta_host = nullptr;
   uint8_t* meta_dev = nullptr;
@@ -221,12 +223,12 @@ int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char*
   return AG_OK;
 }
 
-// GEMM against a weight: choose the N tile, then the matching tensor map.
+// GEMM against a weight: plan (N tile, K splits) for this M, then launch with the matching map.
 cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
-                   cudaStream_t s) {
-  int bn = ag::pick_block_n(M, N);
-  if (bn == 256 && !w.has256) bn = 128;
-  return ag::launch_gemm(a, bn == 256 ? w.box256 : w.box128, M, N, K, bn, ep, 0, s);
+                   cudaStream_t s, float* splitk_ws, int64_t splitk_cap) {
+  ag::GemmPlan p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
+  if (p.bn == 256 && !w.has256) p.bn = 128;
+  return ag::launch_gemm(a, p.bn == 256 ? w.box256 : w.box128, M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws);
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -335,6 +337,8 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   m->part_cap = std::max(4096, c.max_tokens * 4);
   chk(dmalloc(&m->part_o, static_cast<size_t>(m->part_cap) * m->heads_l * m->head_dim));
   chk(dmalloc(&m->part_ml, static_cast<size_t>(m->part_cap) * m->heads_l * 2));
+  m->splitk_cap = int64_t(32) << 20;  // fp32 K-split partials (128 MB)
+  chk(dmalloc(&m->splitk_ws, static_cast<size_t>(m->splitk_cap)));
   // metadata capacity: token arrays, sequence arrays, block table, attention work list
   const size_t max_items = static_cast<size_t>(c.max_tokens) + c.max_seqs + 64 * static_cast<size_t>(ag::num_sms());
   m->meta_cap = align_up(4 * sizeof(int32_t) * T, 256) + align_up(2 * sizeof(int32_t) * (c.max_seqs + 1), 256) +
@@ -367,7 +371,8 @@ void ag_model_destroy(ag_model* m) {
   if (!m) return;
   if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
   void* dev[] = {m->resid, m->xln, m->qbuf, m->attn, m->ffn, m->proj, m->lm_in, m->logits, m->cand_val,
-                 m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev};
+                 m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev,
+                 m->splitk_ws};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (m->meta_host) cudaFreeHost(m->meta_host);
@@ -570,7 +575,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ep.head_dim = m->head_dim;
         ep.block_size = c.block_size;
         ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s, m->splitk_ws, m->splitk_cap));
       }
       {
         ag::AttnParams ap;
@@ -605,7 +610,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           eo.out = m->proj;
         }
         ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s));
+        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap));
       }
       if (tp) {
         {
@@ -628,7 +633,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e1.out = m->ffn;
         e1.ldc = m->ffn_l;
         ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s, m->splitk_ws, m->splitk_cap));
       }
       {
         ag::GemmEpilogue e2;
@@ -642,7 +647,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           e2.out = m->proj;
         }
         ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s));
+        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap));
       }
       if (tp) {
         ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
@@ -671,7 +676,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     float* lg = static_cast<float*>(el.out);
     {
       ProfScope ps(m, AG_K_LMHEAD_GEMM, s, gemm_flops(NL, m->vocab_l, H), gemm_bytes(NL, m->vocab_l, H, 4));
-      AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s));
+      AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s, m->splitk_ws, m->splitk_cap));
     }
     if (!tp) {
       ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 4.0 * NL * m->vocab_l);
@@ -743,10 +748,23 @@ int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, fl
 // ---------------------------------------------------------------- standalone kernels
 int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias, const void* residual,
                      int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32, int32_t M, int32_t N, int32_t K,
-                     int32_t block_n, void* stream) {
+                     int32_t block_n, int32_t k_splits, void* workspace, int64_t workspace_bytes, void* stream) {
   if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");
   if (M < 0 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0) return fail(AG_EINVAL, "need N%32==0, K%8==0");
+  const int64_t cap = workspace ? workspace_bytes / 4 : 0;
+  if (block_n == 0 && k_splits == 0) {
+    const ag::GemmPlan p = ag::plan_gemm(M, N, K, cap);
+    block_n = p.bn;
+    k_splits = p.k_splits;
+  }
   if (block_n == 0) block_n = ag::pick_block_n(M, N);
+  if (k_splits <= 0) k_splits = 1;
+  if (k_splits > 1 && static_cast<int64_t>(k_splits) * M * N > cap)
+    return fail(AG_EALLOC, "split-K workspace too small");
+  {
+    const int nkb = (K + 63) / 64, per = (nkb + k_splits - 1) / k_splits;
+    if ((nkb + per - 1) / per != k_splits) return fail(AG_EINVAL, "k_splits leaves an empty K range");
+  }
   if (block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 128 or 256");
   CUtensorMap ta, tb;
   int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, 128);
@@ -761,7 +779,8 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
   ep.out = D;
   ep.ldc = ldd;
   ep.out_f32 = out_f32;
-  AG_CUDA(ag::launch_gemm(ta, tb, M, N, K, block_n, ep, 0, static_cast<cudaStream_t>(stream)));
+  AG_CUDA(ag::launch_gemm(ta, tb, M, N, K, block_n, ep, 0, static_cast<cudaStream_t>(stream), k_splits,
+                          static_cast<float*>(workspace)));
   return AG_OK;
 }
 

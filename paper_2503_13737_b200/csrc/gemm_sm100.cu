@@ -12,6 +12,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace ag {
 
 namespace {
@@ -119,7 +121,7 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K,
-                        GemmEpilogue ep) {
+                        GemmEpilogue ep, int k_splits, float* __restrict__ partial) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -136,8 +138,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
-  const int num_kb = (K + kBK - 1) / kBK;
+  const int num_kb_total = (K + kBK - 1) / kBK;
+  const int kb_per = (num_kb_total + k_splits - 1) / k_splits;
+  // work unit = (m_blk, k_split, n_blk) with m fastest so CTAs running together share weights
+  const int num_tiles = num_m * num_n * k_splits;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -166,8 +170,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int m_blk = t % num_m;
-        const int n_blk = t / num_m;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int ks = (t / num_m) % k_splits;
+        const int n_blk = t / (num_m * k_splits);
+        const int kb0 = ks * kb_per;
+        const int kb1 = min(num_kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM);
@@ -192,7 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int ks = (t / num_m) % k_splits;
+        const int kb0 = ks * kb_per;
+        const int kb1 = min(num_kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * Cfg::kABytes));
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // +32 bytes along K inside the swizzle atom == +2 in the (addr >> 4) field
-            umma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
           if (++stage == S) {
@@ -220,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_blk = t % num_m;
-      const int n_blk = t / num_m;
+      const int ks = (t / num_m) % k_splits;
+      const int n_blk = t / (num_m * k_splits);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * kBM + ew * 32 + lane;
@@ -230,7 +241,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int col0 = n_blk * BN + c * 32;
-        if (row < M && col0 < N) epilogue_chunk(ep, row, col0, r);
+        if (row < M && col0 < N) {
+          if (k_splits == 1) {
+            epilogue_chunk(ep, row, col0, r);
+          } else {  // fp32 partial of this K split; splitk_reduce_kernel applies the epilogue
+            float* dst = partial + ((size_t)ks * M + row) * N + col0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) st_global_v4(dst + q * 4, r[q * 4], r[q * 4 + 1], r[q * 4 + 2], r[q * 4 + 3]);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -245,6 +264,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+// Sum the K-split fp32 partials of 32 consecutive columns and apply the fused epilogue.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M,
+                                                            int N, GemmEpilogue ep) {
+  const int chunks = N / 32;
+  const int64_t total = static_cast<int64_t>(M) * chunks;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / chunks);
+    const int col0 = static_cast<int>(i - static_cast<int64_t>(row) * chunks) * 32;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+    for (int s = 0; s < splits; ++s) {
+      const float4* src = reinterpret_cast<const float4*>(partial + ((size_t)s * M + row) * N + col0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = src[q];
+        acc[q * 4] += v.x;
+        acc[q * 4 + 1] += v.y;
+        acc[q * 4 + 2] += v.z;
+        acc[q * 4 + 3] += v.w;
+      }
+    }
+    uint32_t r[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[j]);
+    epilogue_chunk(ep, row, col0, r);
   }
 }
 
@@ -294,7 +343,8 @@ int num_sms() {
 
 template <int BN>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
-                             const GemmEpilogue& ep, int max_ctas, cudaStream_t stream) {
+                             const GemmEpilogue& ep, int k_splits, float* partial, int max_ctas,
+                             cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -303,19 +353,56 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int units = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * k_splits;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (tiles < grid) grid = tiles;
-  gemm_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep);
+  if (units < grid) grid = units;
+  gemm_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || k_splits == 1) return e;
+  const int64_t work = static_cast<int64_t>(M) * (N / 32);
+  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+  splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
-                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream) {
+                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial) {
   if (M <= 0) return cudaSuccess;
-  if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, max_ctas, stream);
-  return launch_bn<128>(ta, tb, M, N, K, ep, max_ctas, stream);
+  if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
+  if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+  return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+}
+
+GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats) {
+  // Estimated makespan in "bytes streamed per SM": every unit loads (128 + BN) rows x 64 K per
+  // k-block; units run in ceil(units / SMs) waves; a split adds an fp32 round trip through L2/HBM
+  // spread over the whole chip, and every unit pays a fixed prologue.
+  const int sms = num_sms();
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_kb = (K + kBK - 1) / kBK;
+  GemmPlan best{256, 1};
+  double best_cost = 1e300;
+  for (int bn : {256, 128}) {
+    if (bn == 256 && N % 256 != 0 && N > 256) continue;
+    const int num_n = (N + bn - 1) / bn;
+    for (int splits = 1; splits <= 16; ++splits) {
+      const int kb_per = (num_kb + splits - 1) / splits;
+      const int real_splits = (num_kb + kb_per - 1) / kb_per;
+      if (real_splits != splits) continue;
+      if (splits > 1 && (kb_per < 4 || static_cast<int64_t>(splits) * M * N > partial_capacity_floats)) break;
+      const int64_t units = static_cast<int64_t>(num_m) * num_n * splits;
+      const double waves = static_cast<double>((units + sms - 1) / sms);
+      const double per_unit = kb_per * (128.0 + bn) * kBK * 2.0 + 96.0 * 1024.0;
+      double cost = waves * per_unit;
+      if (splits > 1) cost += static_cast<double>(M) * N * 4.0 * (splits + 1) / sms;
+      if (cost < best_cost * 0.98) {
+        best_cost = cost;
+        best = {bn, splits};
+      }
+    }
+  }
+  return best;
 }
 
 int pick_block_n(int M, int N) {

@@ -34,8 +34,16 @@ int make_tmap_kmajor(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
                      int box_rows);
 int num_sms();
 int pick_block_n(int M, int N);
+// k_splits > 1 writes fp32 partials to `partial` (k_splits * M * N floats) and a reduce kernel
+// applies the epilogue; choose (bn, k_splits) with plan_gemm.
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
-                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream);
+                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits = 1,
+                        float* partial = nullptr);
+struct GemmPlan {
+  int bn;
+  int k_splits;
+};
+GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats);
 
 // embed: out[r] = tok_emb[ids[r]] + pos_emb[positions[r] + pos_offset]
 cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,

@@ -26,9 +26,22 @@ def _need_cuda(*ts: torch.Tensor | None) -> None:
             raise EngineFault("libaccelgen_b200 kernels require CUDA tensors (no CPU fallback)")
 
 
+_WS: dict = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    ws = _WS.get(device)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 64 << 20), dtype=torch.uint8, device=device)
+        _WS[device] = ws
+    return ws
+
+
 def gemm(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, residual: torch.Tensor | None = None,
-         relu: bool = False, out_f32: bool = False, out: torch.Tensor | None = None, block_n: int = 0) -> torch.Tensor:
-    """D = a @ w.T (+bias) (+residual) (relu) on the tcgen05 GEMM; a [M,K], w [N,K] bf16."""
+         relu: bool = False, out_f32: bool = False, out: torch.Tensor | None = None, block_n: int = 0,
+         k_splits: int = 0) -> torch.Tensor:
+    """D = a @ w.T (+bias) (+residual) (relu) on the tcgen05 GEMM; a [M,K], w [N,K] bf16.
+    block_n / k_splits 0 = planned by the library (split-K partials in a cached workspace)."""
     _need_cuda(a, w, bias, residual, out)
     if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ValidationError("gemm operands must be bf16")
@@ -38,10 +51,11 @@ def gemm(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, res
         raise ValidationError(f"K mismatch {K} vs {K2}")
     if out is None:
         out = torch.empty(M, N, device=a.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    ws = _workspace(a.device, 4 * max(1, k_splits, 16) * M * N)
     _lib.check(_lib.load().ag_gemm_bf16(
         a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), _ptr(bias), _ptr(residual),
         residual.stride(0) if residual is not None else 0, int(relu), out.data_ptr(), out.stride(0), int(out_f32),
-        M, N, K, block_n, _stream()))
+        M, N, K, block_n, k_splits, ws.data_ptr(), ws.numel(), _stream()))
     return out
 
 

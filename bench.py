@@ -276,7 +276,12 @@ def run_ours(args):
         "attention": {"ms": attn["ms"], "tflops": attn["flops"] / (attn["ms"] / 1e3) / 1e12 if attn["ms"] else 0.0,
                       "gbs": attn["bytes"] / (attn["ms"] / 1e3) / 1e9 if attn["ms"] else 0.0},
         "kernel_share": shares,
+        "host_ms_per_step": {"pre": 1e3 * sum(r.host_pre_s for r in recs) / K,
+                             "execute_wall": 1e3 * sum(r.wall_s for r in recs) / K,
+                             "post": 1e3 * sum(r.host_post_s for r in recs) / K,
+                             "device_forward": 1e3 * dev_s / K, "wall_total": 1e3 * wall / K},
         "clocks": clocks,
+        "gemm_plans": " ".join(f"{k}:{mb}:{bn}x{ks}" for k, mb, bn, ks in ex.gemm_plans()),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mcfg, batches, world)

@@ -133,6 +133,12 @@ AG_API int32_t ag_model_forward(ag_model* m, const ag_step* step, int32_t* out_t
 AG_API int32_t ag_model_stage_step(ag_model* m, const ag_step* step, void* stream);
 AG_API int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* logits_out, void* stream);
 
+/* Time every candidate (BLOCK_N, K-split) plan of the model's GEMM shapes (QKV, out, FC1, FC2,
+ * LM head) over M buckets up to max_tokens on this GPU and keep the fastest; later forwards use
+ * the table.  ~1 s at model load.  get_gemm_plans writes (kind, m_bucket, block_n, k_splits) rows. */
+AG_API int32_t ag_model_autotune(ag_model* m, void* stream);
+AG_API int32_t ag_model_get_gemm_plans(ag_model* m, int32_t* out_rows4, int32_t cap);
+
 /* Per-kernel-class CUDA-event profiling of ag_model_forward (on = 1 resets the counters).
  * get_profile fills up to n entries per class: summed ms, algorithmic FLOPs and HBM bytes, launches. */
 AG_API int32_t ag_model_set_profiling(ag_model* m, int32_t on);

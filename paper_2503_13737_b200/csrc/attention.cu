@@ -25,7 +25,11 @@ constexpr int kRowBytes = kHD * 2;
 constexpr int kStageBytes = 2 * kStageTok * kRowBytes;  // K + V = 32 KB
 constexpr int kStages = 2;
 constexpr int kAttnThreads = 128;
-constexpr int kAttnSmem = kStages * kStageBytes;  // 64 KB (>= decode merge scratch 32 KB + 512 B)
+constexpr int kDecHalf = 16;                              // tokens per decode ring slot (half page)
+constexpr int kDecSlotBytes = 2 * kDecHalf * kRowBytes;   // K + V = 8 KB
+constexpr int kDecStages = 3;
+constexpr int kDecWarpBytes = kDecStages * kDecSlotBytes;  // 24 KB per warp
+constexpr int kAttnSmem = 4 * kDecWarpBytes;               // 96 KB >= tile path 64 KB
 constexpr float kLog2e = 1.4426950408889634f;
 
 AG_DEVICE void cp_async16(uint32_t dst, const void* src) {
@@ -164,12 +168,146 @@ AG_DEVICE void attend_stage(uint32_t sK, uint32_t sV, int tok0, const uint32_t (
   }
 }
 
+// ---------------------------------------------------------------- single-row (decode) path
+// One warp streams the KV range of one (sequence, head, split) through its own 3-slot cp.async
+// ring of 16-token half pages (8 KB: K then V), independent of the other warps of the CTA.
+//   QK^T: lanes 0-15 / 16-31 take token 2i / 2i+1 of a slot, 8 dims (one 16-B chunk) each, and
+//         reduce over their 16 lanes -> every lane holds the score of its token pair member;
+//   PV:   lane l owns output dims 4l..4l+3 and walks the slot's 16 tokens (coalesced 256-B rows).
+AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head, uint8_t* wsmem) {
+  const int lane = lane_id();
+  const int q0 = p.cu_q[it.seq];
+  const int tok_row = q0 + it.q_start;
+  const int qpos = p.ctx_len[it.seq] + it.q_start;
+  const int kv_end = min(it.kv_end, qpos + 1);
+  const int chunk = lane & 15;
+  // q chunk for the QK phase (pre-scaled by head_dim^-0.5 in the QKV epilogue), folded with log2e
+  float qv[8];
+  {
+    const uint4 w = *reinterpret_cast<const uint4*>(p.q + static_cast<int64_t>(tok_row) * p.ldq + head * kHD + chunk * 8);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float2 f = unpack_bf16x2(ws[h]);
+      qv[2 * h] = f.x * kLog2e;
+      qv[2 * h + 1] = f.y * kLog2e;
+    }
+  }
+  const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
+  const int64_t page_elems = static_cast<int64_t>(p.heads) * kPage * kHD;
+  const int64_t head_off = static_cast<int64_t>(head) * kPage * kHD;
+  const int h0 = it.kv_start / kDecHalf;
+  const int h1 = (kv_end + kDecHalf - 1) / kDecHalf;
+  const uint32_t sbase = smem_u32(wsmem);
+
+  auto issue = [&](int h, int slot) {
+    const int page = (h * kDecHalf) / kPage;
+    const int tok0 = (h * kDecHalf) % kPage;
+    const int64_t base = static_cast<int64_t>(bt[page]) * page_elems + head_off + static_cast<int64_t>(tok0) * kHD;
+    const uint32_t sk = sbase + slot * kDecSlotBytes;
+    const uint32_t sv = sk + kDecHalf * kRowBytes;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // 16 rows x 16 chunks = 256 x 16 B per tensor, 8 per lane
+      const int id = lane + 32 * i;
+      cp_async16(sk + id * 16, p.kcache + base + id * 8);
+      cp_async16(sv + id * 16, p.vcache + base + id * 8);
+    }
+  };
+
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  float m = -INFINITY, l = 0.f;
+  int issued = h0;
+  for (int k = 0; k < kDecStages - 1; ++k) {
+    if (issued < h1) issue(issued, (issued - h0) % kDecStages);
+    ++issued;
+    cp_async_commit();
+  }
+  for (int h = h0; h < h1; ++h) {
+    if (issued < h1) issue(issued, (issued - h0) % kDecStages);
+    ++issued;
+    cp_async_commit();
+    cp_async_wait<kDecStages - 1>();
+    __syncwarp();
+    const int slot = (h - h0) % kDecStages;
+    const uint8_t* sk = wsmem + slot * kDecSlotBytes;
+    const uint8_t* sv = sk + kDecHalf * kRowBytes;
+    // scores: lane keeps token (lane & 15)
+    float s_mine = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kDecHalf / 2; ++i) {
+      const int t = 2 * i + (lane >> 4);
+      const uint4 w = *reinterpret_cast<const uint4*>(sk + t * kRowBytes + chunk * 16);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      float d = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        const float2 f = unpack_bf16x2(ws[hh]);
+        d = fmaf(qv[2 * hh], f.x, d);
+        d = fmaf(qv[2 * hh + 1], f.y, d);
+      }
+#pragma unroll
+      for (int o2 = 8; o2 > 0; o2 >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o2);
+      // lanes 0-15 now hold token 2i, lanes 16-31 token 2i+1; lane keeps token (lane & 15)
+      const float other = __shfl_sync(0xffffffffu, d, (lane & 1) * 16);
+      if ((lane & 15) >> 1 == i) s_mine = other;
+    }
+    const int pos = h * kDecHalf + (lane & 15);
+    if (pos >= kv_end || pos < it.kv_start) s_mine = -INFINITY;
+    float mx = s_mine;
+#pragma unroll
+    for (int o2 = 8; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+    const float mnew = fmaxf(m, mx);
+    const float mref = mnew == -INFINITY ? 0.f : mnew;
+    const float alpha = exp2f(m - mref);
+    const float pe = exp2f(s_mine - mref);
+    float ps = pe;
+#pragma unroll
+    for (int o2 = 8; o2 > 0; o2 >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o2);
+    l = l * alpha + ps;
+    m = mnew;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] *= alpha;
+#pragma unroll
+    for (int t = 0; t < kDecHalf; ++t) {
+      const float pt = __shfl_sync(0xffffffffu, pe, t);
+      const uint2 w = *reinterpret_cast<const uint2*>(sv + t * kRowBytes + lane * 8);
+      const float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y);
+      o[0] = fmaf(pt, a.x, o[0]);
+      o[1] = fmaf(pt, a.y, o[1]);
+      o[2] = fmaf(pt, b.x, o[2]);
+      o[3] = fmaf(pt, b.y, o[3]);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  if (it.part_row < 0) {
+    __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_row) * p.ldo + head * kHD + lane * 4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv));
+  } else {
+    const int64_t prow = static_cast<int64_t>(it.part_row) * p.heads + head;
+    *reinterpret_cast<float4*>(p.part_o + prow * kHD + lane * 4) = make_float4(o[0] * inv, o[1] * inv, o[2] * inv, o[3] * inv);
+    if (lane == 0) {
+      p.part_ml[prow * 2] = m;
+      p.part_ml[prow * 2 + 1] = l;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kAttnThreads)
-    mixed_attention_kernel(AttnParams p, const AttnItem* __restrict__ items) {
+    mixed_attention_kernel(AttnParams p, const AttnItem* __restrict__ items, int n_tile_items, int n_row_items) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const AttnItem it = items[blockIdx.x];
-  const int head = blockIdx.y;
   const int warp = threadIdx.x >> 5;
+  const int n_tile_ctas = n_tile_items * p.heads;
+  if (static_cast<int>(blockIdx.x) >= n_tile_ctas) {
+    const int u = (blockIdx.x - n_tile_ctas) * 4 + warp;  // (item, head) unit of this warp
+    if (u >= n_row_items * p.heads) return;
+    const AttnItem itr = items[n_tile_items + u / p.heads];
+    decode_row_warp(p, itr, u % p.heads, smem + warp * kDecWarpBytes);
+    return;
+  }
+  const AttnItem it = items[blockIdx.x / p.heads];
+  const int head = blockIdx.x % p.heads;
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const bool decode_mode = it.q_rows <= 16;
@@ -357,9 +495,10 @@ __global__ void attn_combine_kernel(AttnParams p, const AttnCombine* __restrict_
 
 }  // namespace
 
-cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_items,
+cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_tile_items, int n_row_items,
                              const AttnCombine* combines, int n_combines, cudaStream_t stream) {
   if (p.block_size != kPage) return cudaErrorInvalidValue;
+  const int n_items = n_tile_items + n_row_items;
   if (n_items > 0) {
     static bool attr = false;
     if (!attr) {
@@ -368,7 +507,8 @@ cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_i
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    mixed_attention_kernel<<<dim3(n_items, p.heads), kAttnThreads, kAttnSmem, stream>>>(p, items);
+    const int ctas = n_tile_items * p.heads + (n_row_items * p.heads + 3) / 4;
+    mixed_attention_kernel<<<ctas, kAttnThreads, kAttnSmem, stream>>>(p, items, n_tile_items, n_row_items);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -73,58 +73,85 @@ NcclApi& nccl() {
 
 // ---------------------------------------------------------------- attention work list
 struct AttnWork {
-  std::vector<AttnItem> items;
+  std::vector<AttnItem> items;  // [tile items (q_rows > 1)] + [single-row items]
   std::vector<AttnCombine> combines;
+  int n_tile = 0, n_row = 0;
   int part_rows = 0;
 };
 
-// Tile every sequence's new tokens into <=64-row query tiles (<=16 rows run in decode mode) and
-// split long KV ranges so that ~4 CTAs per SM of work exist; splits are multiples of 64 tokens.
+// Tile every sequence's new tokens: >1-row pieces become <=64-row tensor-core tiles (<=16 rows run
+// in the 4-warp small-tile mode), single-row pieces (decode tokens) become warp-level streaming
+// items.  Long KV ranges are split (split-KV) so that tiles give ~4 CTAs/SM and single-row items
+// ~16 warps/SM of work; splits are multiples of 64 tokens and merged by attn_combine_kernel.
 void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, int heads, int part_cap,
                           AttnWork& w) {
   w.items.clear();
   w.combines.clear();
   w.part_rows = 0;
-  struct Tile {
+  struct Piece {
     int seq, qs, rows, kv_hi;
-    double cost;
   };
-  std::vector<Tile> tiles;
-  double total = 0.0;
+  std::vector<Piece> tiles, rows1;
+  double tile_work = 0.0, row_work = 0.0;
   for (int b = 0; b < B; ++b) {
     const int q = cu_q[b + 1] - cu_q[b];
     if (q <= 0) continue;
+    if (q == 1) {
+      rows1.push_back({b, 0, 1, ctx_len[b] + 1});
+      row_work += ctx_len[b] + 1;
+      continue;
+    }
     const int T = q <= 16 ? 16 : 64;
     for (int qs = 0; qs < q; qs += T) {
-      const int rows = std::min(T, q - qs);
-      const int kv_hi = ctx_len[b] + qs + rows;
-      const double c = static_cast<double>(kv_hi) * (rows > 16 ? 4.0 : 1.0);
-      tiles.push_back({b, qs, rows, kv_hi, c});
-      total += c;
+      const int r = std::min(T, q - qs);
+      tiles.push_back({b, qs, r, ctx_len[b] + qs + r});
+      tile_work += static_cast<double>(ctx_len[b] + qs + r) * (r > 16 ? 4.0 : 1.0);
     }
   }
-  const int desired = std::max(1, (ag::num_sms() * 4 + heads - 1) / heads);
-  const double per_item = std::max(1.0, total / desired);
-  for (const Tile& t : tiles) {
-    int n_split = static_cast<int>(std::ceil(t.cost / per_item));
-    n_split = std::max(1, std::min(n_split, (t.kv_hi + 255) / 256));
-    int split = (t.kv_hi + n_split - 1) / n_split;
-    split = (split + 63) / 64 * 64;
-    n_split = (t.kv_hi + split - 1) / split;
+  const int sms = ag::num_sms();
+  auto emit = [&](const Piece& t, int n_split, int split, std::vector<AttnItem>& out) {
     if (n_split > 1 && w.part_rows + n_split * t.rows > part_cap) n_split = 1;
     if (n_split == 1) {
-      w.items.push_back({t.seq, t.qs, t.rows, 0, t.kv_hi, -1, 0, 0});
-      continue;
+      out.push_back({t.seq, t.qs, t.rows, 0, t.kv_hi, -1, 0, 0});
+      return;
     }
     const int base = w.part_rows;
     for (int s = 0; s < n_split; ++s) {
       const int a = s * split;
-      const int e = std::min(t.kv_hi, a + split);
-      w.items.push_back({t.seq, t.qs, t.rows, a, e, base + s * t.rows, 0, 0});
+      out.push_back({t.seq, t.qs, t.rows, a, std::min(t.kv_hi, a + split), base + s * t.rows, 0, 0});
     }
     w.combines.push_back({cu_q[t.seq] + t.qs, t.rows, base, n_split});
     w.part_rows += n_split * t.rows;
+  };
+  auto split_of = [](int kv_hi, double per_item, double weight, int min_len, int& n_split, int& split) {
+    n_split = static_cast<int>(std::ceil(kv_hi * weight / per_item));
+    n_split = std::max(1, std::min(n_split, (kv_hi + min_len - 1) / min_len));
+    split = ((kv_hi + n_split - 1) / n_split + 63) / 64 * 64;
+    n_split = (kv_hi + split - 1) / split;
+  };
+  std::vector<AttnItem> tile_items, row_items;
+  {
+    const int desired = std::max(1, (sms * 4 + heads - 1) / heads);
+    const double per_item = std::max(1.0, tile_work / desired);
+    for (const Piece& t : tiles) {
+      int n, sp;
+      split_of(t.kv_hi, per_item, t.rows > 16 ? 4.0 : 1.0, 256, n, sp);
+      emit(t, n, sp, tile_items);
+    }
   }
+  {
+    const int desired = std::max(1, (sms * 16 + heads - 1) / heads);
+    const double per_item = std::max(512.0, row_work / desired);
+    for (const Piece& t : rows1) {
+      int n, sp;
+      split_of(t.kv_hi, per_item, 1.0, 512, n, sp);
+      emit(t, n, sp, row_items);
+    }
+  }
+  w.n_tile = static_cast<int>(tile_items.size());
+  w.n_row = static_cast<int>(row_items.size());
+  w.items = std::move(tile_items);
+  w.items.insert(w.items.end(), row_items.begin(), row_items.end());
 }
 
 }  // namespace
@@ -134,6 +161,14 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
 struct WeightMap {
   CUtensorMap box128, box256;
   bool has256 = false;
+};
+
+// Autotuned (BLOCK_N, k_splits) per GEMM kind and M bucket (ag_model_autotune).
+enum GemmKind { kGemmQkv = 0, kGemmOut, kGemmFc1, kGemmFc2, kGemmLm, kGemmKinds };
+struct GemmTable {
+  std::vector<int> m_bucket;                // ascending
+  std::vector<ag::GemmPlan> plan[kGemmKinds];
+  bool ready = false;
 };
 
 struct LayerState {
@@ -165,6 +200,7 @@ struct ag_model {
   int part_cap = 0;
   float* splitk_ws = nullptr;
   int64_t splitk_cap = 0;
+  GemmTable tune;
   // metadata: one pinned host buffer mirrored by one device buffer
   uint8_t* meta_host = nullptr;
   uint8_t* meta_dev = nullptr;
@@ -173,7 +209,7 @@ struct ag_model {
   CUtensorMap tm_xln, tm_attn, tm_ffn, tm_lm_in;
   WeightMap tm_lm_w;
   // staged step
-  int S = 0, B = 0, n_logit = 0, bt_stride = 0, n_items = 0, n_comb = 0;
+  int S = 0, B = 0, n_logit = 0, bt_stride = 0, n_items = 0, n_comb = 0, n_tile_items = 0, n_row_items = 0;
   const int32_t *d_ids = nullptr, *d_pos = nullptr, *d_cuq = nullptr, *d_ctx = nullptr, *d_bt = nullptr,
                 *d_slot = nullptr, *d_lrows = nullptr;
   const AttnItem* d_items = nullptr;
@@ -223,10 +259,22 @@ int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char*
   return AG_OK;
 }
 
-// GEMM against a weight: plan (N tile, K splits) for this M, then launch with the matching map.
+// GEMM against a weight: (N tile, K splits) from the autotuned table for this M bucket (or the
+// analytic planner before autotune), then launch with the matching tensor map.
 cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
-                   cudaStream_t s, float* splitk_ws, int64_t splitk_cap) {
-  ag::GemmPlan p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
+                   cudaStream_t s, float* splitk_ws, int64_t splitk_cap, const GemmTable* tune = nullptr,
+                   int kind = -1) {
+  ag::GemmPlan p{0, 0};
+  if (tune && tune->ready && kind >= 0) {
+    for (size_t i = 0; i < tune->m_bucket.size(); ++i) {
+      if (M <= tune->m_bucket[i] || i + 1 == tune->m_bucket.size()) {
+        p = tune->plan[kind][i];
+        break;
+      }
+    }
+    if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
+  }
+  if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
   if (p.bn == 256 && !w.has256) p.bn = 128;
   return ag::launch_gemm(a, p.bn == 256 ? w.box256 : w.box128, M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws);
 }
@@ -525,6 +573,8 @@ int32_t ag_model_stage_step(ag_model* m, const ag_step* st, void* stream) {
   m->n_logit = NL;
   m->bt_stride = bts;
   m->n_items = static_cast<int>(m->work.items.size());
+  m->n_tile_items = m->work.n_tile;
+  m->n_row_items = m->work.n_row;
   m->n_comb = static_cast<int>(m->work.combines.size());
   return AG_OK;
 }
@@ -575,7 +625,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ep.head_dim = m->head_dim;
         ep.block_size = c.block_size;
         ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s, m->splitk_ws, m->splitk_cap));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmQkv));
       }
       {
         ag::AttnParams ap;
@@ -595,7 +645,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ap.block_size = c.block_size;
         ProfScope ps(m, AG_K_ATTENTION, s, m->attn_flops_step, m->attn_bytes_step);
         if (m->n_comb > 0) m->launches_last += 1;
-        AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_items, m->d_comb, m->n_comb, s));
+        AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_tile_items, m->n_row_items, m->d_comb, m->n_comb, s));
       }
       {
         // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
@@ -610,7 +660,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           eo.out = m->proj;
         }
         ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap));
+        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmOut));
       }
       if (tp) {
         {
@@ -633,7 +683,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e1.out = m->ffn;
         e1.ldc = m->ffn_l;
         ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s, m->splitk_ws, m->splitk_cap));
+        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc1));
       }
       {
         ag::GemmEpilogue e2;
@@ -647,7 +697,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           e2.out = m->proj;
         }
         ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap));
+        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc2));
       }
       if (tp) {
         ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
@@ -676,7 +726,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     float* lg = static_cast<float*>(el.out);
     {
       ProfScope ps(m, AG_K_LMHEAD_GEMM, s, gemm_flops(NL, m->vocab_l, H), gemm_bytes(NL, m->vocab_l, H, 4));
-      AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s, m->splitk_ws, m->splitk_cap));
+      AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmLm));
     }
     if (!tp) {
       ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 4.0 * NL * m->vocab_l);
@@ -723,6 +773,98 @@ int32_t ag_model_get_profile(ag_model* m, double* ms, double* flops, double* byt
     if (counts) counts[i] = m->prof_count[i];
   }
   return AG_OK;
+}
+
+int32_t ag_model_autotune(ag_model* m, void* stream) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  for (int l = 0; l < m->cfg.num_layers; ++l)
+    if (!m->layers[l].ready) return fail(AG_EINVAL, "set weights before autotune");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ag_model_config& c = m->cfg;
+  const int H = c.hidden;
+  GemmTable& t = m->tune;
+  t.m_bucket.clear();
+  for (int mb : {16, 32, 64, 128, 192, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288, 16384})
+    if (mb < c.max_tokens) t.m_bucket.push_back(mb);
+  t.m_bucket.push_back(c.max_tokens);
+  const size_t T = align_up(static_cast<size_t>(c.max_tokens), 128);
+  AG_CUDA(cudaMemsetAsync(m->xln, 0, T * H * 2, s));
+  AG_CUDA(cudaMemsetAsync(m->attn, 0, T * m->hq * 2, s));
+  AG_CUDA(cudaMemsetAsync(m->ffn, 0, T * m->ffn_l * 2, s));
+  AG_CUDA(cudaMemsetAsync(m->lm_in, 0, align_up(c.max_seqs, 128) * H * 2, s));
+  const LayerState& L0 = m->layers[0];
+  struct Shape {
+    const CUtensorMap* a;
+    const WeightMap* w;
+    int N, K, mcap;
+    void* out;
+    int out_f32;
+  } shapes[kGemmKinds] = {
+      {&m->tm_xln, &L0.tm_qkv, 3 * m->hq, H, c.max_tokens, m->ffn, 0},
+      {&m->tm_attn, &L0.tm_out, H, m->hq, c.max_tokens, m->ffn, 0},
+      {&m->tm_xln, &L0.tm_fc1, m->ffn_l, H, c.max_tokens, m->ffn, 0},
+      {&m->tm_ffn, &L0.tm_fc2, H, m->ffn_l, c.max_tokens, m->proj, 0},
+      {&m->tm_lm_in, &m->tm_lm_w, m->vocab_l, H, c.max_seqs, m->logits, 1},
+  };
+  const ag::GemmPlan cands[] = {{256, 1}, {128, 1}, {256, 2}, {128, 2}, {256, 3}, {256, 4}, {128, 4},
+                                {256, 6}, {256, 8}, {128, 8}};
+  cudaEvent_t e0, e1;
+  AG_CUDA(cudaEventCreate(&e0));
+  AG_CUDA(cudaEventCreate(&e1));
+  for (int k = 0; k < kGemmKinds; ++k) {
+    t.plan[k].assign(t.m_bucket.size(), ag::GemmPlan{256, 1});
+    const Shape& sh = shapes[k];
+    for (size_t b = 0; b < t.m_bucket.size(); ++b) {
+      const int M = std::min(t.m_bucket[b], sh.mcap);
+      ag::GemmEpilogue ep;
+      ep.out = sh.out;
+      ep.ldc = sh.N;
+      ep.out_f32 = sh.out_f32;
+      float best = 1e30f;
+      for (const ag::GemmPlan& p : cands) {
+        if (p.bn == 256 && !sh.w->has256) continue;
+        const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
+        if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
+        if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
+        const CUtensorMap& wm = p.bn == 256 ? sh.w->box256 : sh.w->box128;
+        for (int rep = 0; rep < 2; ++rep)
+          AG_CUDA(ag::launch_gemm(*sh.a, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws));
+        const int iters = 5;
+        AG_CUDA(cudaEventRecord(e0, s));
+        for (int rep = 0; rep < iters; ++rep)
+          AG_CUDA(ag::launch_gemm(*sh.a, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws));
+        AG_CUDA(cudaEventRecord(e1, s));
+        AG_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        AG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best * 0.985f) {  // prefer earlier (simpler) plans on near-ties
+          best = ms;
+          t.plan[k][b] = p;
+        }
+      }
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.ready = true;
+  return AG_OK;
+}
+
+int32_t ag_model_get_gemm_plans(ag_model* m, int32_t* out, int32_t cap) {
+  // rows of (kind, m_bucket, block_n, k_splits); returns the row count
+  if (!m || !m->tune.ready) return 0;
+  int n = 0;
+  for (int k = 0; k < kGemmKinds; ++k)
+    for (size_t b = 0; b < m->tune.m_bucket.size(); ++b) {
+      if (n < cap) {
+        out[4 * n] = k;
+        out[4 * n + 1] = m->tune.m_bucket[b];
+        out[4 * n + 2] = m->tune.plan[k][b].bn;
+        out[4 * n + 3] = m->tune.plan[k][b].k_splits;
+      }
+      ++n;
+    }
+  return n;
 }
 
 int64_t ag_model_last_launches(ag_model* m) { return m ? m->launches_last : -1; }
@@ -829,8 +971,7 @@ int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const
   ap.part_ml = ap.part_o + static_cast<int64_t>(part_cap) * heads * 128;
   ap.heads = heads;
   ap.block_size = block_size;
-  AG_CUDA(ag::launch_attention(ap, reinterpret_cast<const AttnItem*>(ws),
-                               static_cast<int>(w.items.size()),
+  AG_CUDA(ag::launch_attention(ap, reinterpret_cast<const AttnItem*>(ws), w.n_tile, w.n_row,
                                reinterpret_cast<const AttnCombine*>(ws + align_up(ib, 256)),
                                static_cast<int>(w.combines.size()), s));
   // the host work vectors must outlive the async copies

@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      const uint64_t pol_w = policy_evict_last();
+      // activations are re-read by every N tile -> keep in L2; weights of a small-M GEMM are
+      // streamed once -> evict first (large M reuses a weight tile across concurrent m-blocks)
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_w = num_m <= 2 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
-          tma_load_2d(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM);
+          tma_load_2d_hint(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM, pol_a);
           tma_load_2d_hint(sB + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage], kb * kBK, n_blk * BN,
                            pol_w);
           if (++stage == S) {

@@ -98,7 +98,8 @@ struct AttnParams {
   int block_size;
 };
 
-cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_items,
+// items = [n_tile_items query tiles (q_rows > 1)] + [n_row_items single-row (decode) items]
+cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_tile_items, int n_row_items,
                              const AttnCombine* combines, int n_combines, cudaStream_t stream);
 
 // argmax over rows of logits (f32), optional vocab offset; writes (value, index) pairs

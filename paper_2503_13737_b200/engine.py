@@ -164,6 +164,8 @@ class IterationRecord:
     events: int = 0
     events_met: int = 0
     slo_tokens: int = 0   # tokens of this forward whose request met (or is on track for) its deadline
+    host_pre_s: float = 0.0   # admit + order + plan + allocate + pack (before executor.execute)
+    host_post_s: float = 0.0  # emission + re-enqueue (after executor.execute)
 
 
 @dataclass
@@ -393,6 +395,7 @@ class Engine:
 
         # ---- execute and advance the clock
         t_host = time.perf_counter()
+        pre_s = t_host - t_step0
         res = self.executor.execute(batch)
         wall = time.perf_counter() - t_host
         if self.clock_mode == "virtual":
@@ -410,7 +413,8 @@ class Engine:
                              forward_size=plan.forward_size, token_budget=plan.token_budget,
                              num_seqs=len(plan.selections), num_decode=0,
                              allocated_tokens=self.pool.allocated_tokens, preemptions=len(plan.preempted),
-                             device_s=res.device_s, wall_s=wall)
+                             device_s=res.device_s, wall_s=wall, host_pre_s=pre_s)
+        t_post = time.perf_counter()
         tok_by_id = dict(zip(logit_ids, res.token_ids.tolist()))
         selected = set()
         finished = []
@@ -471,6 +475,7 @@ class Engine:
         if finished:
             gone = set(finished)
             self.queue = [e for e in self.queue if e.request_id not in gone]
+        it.host_post_s = time.perf_counter() - t_post
         self.metrics.iterations.append(it)
         return it
 

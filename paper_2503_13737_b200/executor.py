@@ -29,7 +29,7 @@ class CudaExecutor:
     def __init__(self, cfg: OPTConfig, num_blocks: int, *, max_tokens: int = 4096, max_seqs: int = 512,
                  max_blocks_per_seq: int | None = None, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
                  init: str = "opt", weights: dict | None = None, device: int | None = None,
-                 parity_logits: bool = False, nccl_uid: bytes | None = None):
+                 parity_logits: bool = False, nccl_uid: bytes | None = None, autotune: bool = True):
         if not torch.cuda.is_available():
             raise EngineFault("CudaExecutor needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -72,6 +72,9 @@ class CudaExecutor:
                 raise EngineFault("tp_size > 1 needs the NCCL unique id broadcast by rank 0")
             buf = C.create_string_buffer(bytes(nccl_uid), 128)
             _lib.check(self.lib.ag_model_init_tp(handle, buf))
+        if autotune:
+            with torch.cuda.device(self.device):
+                _lib.check(self.lib.ag_model_autotune(handle, torch.cuda.current_stream(self.device).cuda_stream))
         self._dev_ms = C.c_float(0.0)
         self._swapped: dict[int, torch.Tensor] = {}
         self.logits_buf = torch.empty(max_seqs, cfg.vocab // tp_size, dtype=torch.float32, device=self.device) \
@@ -91,6 +94,12 @@ class CudaExecutor:
         _lib.check(self.lib.ag_model_get_profile(self.handle, ms, fl, by, cnt, n))
         return {name: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
                 for i, name in enumerate(_lib.PROF_CLASSES)}
+
+    def gemm_plans(self) -> list[tuple[str, int, int, int]]:
+        kinds = ("qkv", "out", "fc1", "fc2", "lm_head")
+        buf = (C.c_int32 * (4 * 512))()
+        n = int(self.lib.ag_model_get_gemm_plans(self.handle, buf, 512))
+        return [(kinds[buf[4 * i]], buf[4 * i + 1], buf[4 * i + 2], buf[4 * i + 3]) for i in range(min(n, 512))]
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -260,6 +260,8 @@ def run_ours(args):
                    "forward_tokens_per_step": tokens / K, "l2": "inputs larger than L2 (26 GB weights/step)",
                    "clock": "wall (live)"},
         "iter_slo_attainment": met / events if events else None,
+        "preemptions_in_window": sum(r.preemptions for r in recs),
+        "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,
         "token_events": events,
         "forward_tokens_per_s": tokens / dev_s if dev_s > 0 else 0.0,
         "e2e": {"value": slo_tokens / wall if wall > 0 else 0.0, "unit": UNIT,

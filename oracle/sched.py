@@ -176,10 +176,11 @@ class OracleScheduler:
         preempted = []
         while B and (s_f > s_b or used > free):
             v = max(B, key=lambda m: (tr[m[0].rid], pos[m[0].rid]))
+            kv_short = used > free
             B.remove(v)
             s_f -= v[1]
             used -= v[2]
-            if v[0].rid in pool.tables:
+            if kv_short and v[0].rid in pool.tables:
                 preempted.append(v[0].rid)
                 free += len(pool.tables[v[0].rid])
             else:
@@ -209,7 +210,7 @@ class OracleScheduler:
                         c = 1
                     blk = pool.need(r, c)
                     if c <= a_c and blk * pool.b <= a_m:
-                        cands.append((math.hypot(a_c - c, a_m - blk * pool.b), i, r, c, blk))
+                        cands.append(((a_c - c) ** 2 + (a_m - blk * pool.b) ** 2, i, r, c, blk))
                 if not cands:
                     break
                 _, _, r, c, blk = min(cands, key=lambda x: (x[0], x[1]))

@@ -159,8 +159,9 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
 // ---------------------------------------------------------------- model object
 // A weight operand needs one tensor map per N-tile width (the TMA box must equal BLOCK_N).
 struct WeightMap {
-  CUtensorMap box128, box256;
+  CUtensorMap box64, box128, box256;
   bool has256 = false;
+  const CUtensorMap& box(int bn) const { return bn == 256 ? box256 : (bn == 64 ? box64 : box128); }
 };
 
 // Autotuned (BLOCK_N, k_splits) per GEMM kind and M bucket (ag_model_autotune).
@@ -253,6 +254,7 @@ int32_t tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t k, int box_r
 }
 
 int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char* what) {
+  AG_TRY(tmap(&w->box64, ptr, rows, k, 64, what));
   AG_TRY(tmap(&w->box128, ptr, rows, k, 128, what));
   w->has256 = rows % 256 == 0;
   if (w->has256) AG_TRY(tmap(&w->box256, ptr, rows, k, 256, what));
@@ -276,7 +278,7 @@ cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K
   }
   if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
   if (p.bn == 256 && !w.has256) p.bn = 128;
-  return ag::launch_gemm(a, p.bn == 256 ? w.box256 : w.box128, M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws);
+  return ag::launch_gemm(a, w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws);
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -806,8 +808,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       {&m->tm_ffn, &L0.tm_fc2, H, m->ffn_l, c.max_tokens, m->proj, 0},
       {&m->tm_lm_in, &m->tm_lm_w, m->vocab_l, H, c.max_seqs, m->logits, 1},
   };
-  const ag::GemmPlan cands[] = {{256, 1}, {128, 1}, {256, 2}, {128, 2}, {256, 3}, {256, 4}, {128, 4},
-                                {256, 6}, {256, 8}, {128, 8}};
+  const ag::GemmPlan cands[] = {{256, 1}, {128, 1}, {64, 1}, {256, 2}, {128, 2}, {64, 2}, {256, 3},
+                                {256, 4}, {128, 4}, {64, 4}, {256, 6}, {128, 6}, {256, 8}, {128, 8}};
   cudaEvent_t e0, e1;
   AG_CUDA(cudaEventCreate(&e0));
   AG_CUDA(cudaEventCreate(&e1));
@@ -826,7 +828,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
         if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
         if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
-        const CUtensorMap& wm = p.bn == 256 ? sh.w->box256 : sh.w->box128;
+        const CUtensorMap& wm = sh.w->box(p.bn);
         for (int rep = 0; rep < 2; ++rep)
           AG_CUDA(ag::launch_gemm(*sh.a, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws));
         const int iters = 5;
@@ -907,7 +909,7 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
     const int nkb = (K + 63) / 64, per = (nkb + k_splits - 1) / k_splits;
     if ((nkb + per - 1) / per != k_splits) return fail(AG_EINVAL, "k_splits leaves an empty K range");
   }
-  if (block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 128 or 256");
+  if (block_n != 64 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 64, 128 or 256");
   CUtensorMap ta, tb;
   int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, 128);
   if (r) return fail(AG_EINVAL, "tensor map A failed (alignment?)");

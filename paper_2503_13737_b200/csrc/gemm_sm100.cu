@@ -24,7 +24,7 @@ constexpr int kThreads = 256;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -374,6 +374,7 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
   if (M <= 0) return cudaSuccess;
   if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
   if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+  if (bn == 64) return launch_bn<64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
 }
 

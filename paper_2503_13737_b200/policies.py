@@ -13,14 +13,16 @@ ambiguity pinned once (SURVEY §8c'):
 * Algorithm 1: urgent entries join B in queue order; a TG or preempted TG task takes 1 token, a
   pending prompt takes min(remaining, max(1, S_b - S_f - R)) tokens where R counts the urgent
   TG tasks not yet placed (sequential token selection, PAPER §4.2, with the returned decodes
-  "retained in the batch as much as possible", PAPER §4.4).  While S_f > S_b or B's block demand exceeds the free blocks, the
-  member with max T_r (ties: later queue position) leaves B; if it holds blocks it is preempted
-  (swapped out, freeing them), otherwise it is deferred.
+  "retained in the batch as much as possible", PAPER §4.4).  While S_f > S_b or B's block demand
+  exceeds the free blocks, the member with max T_r (ties: later queue position) leaves B; only
+  when the KV blocks are the deficit and it holds blocks is it preempted (swapped out, freeing
+  them) -- a token-budget deficit merely defers it with its KV resident.
 * Algorithm 2 (select_requests): window = non-urgent entries with T_r <= T_r^1 + gamma.  Every
   pending prompt in the window (short or long, PAPER §4.2 "regardless of their associated
   requests") is offered as a chunk min(remaining, A_c, tokens fitting A_m); TG / preempted TG
   tasks are offered with D_c = 1.  D_m is blocks x b (block granularity).  The
-  feasible candidate minimising sqrt((A_c-D_c)^2 + (A_m-D_m)^2) is taken (ties: earlier queue
+  feasible candidate minimising (A_c-D_c)^2 + (A_m-D_m)^2 (exact integers; same order as the
+  Euclidean distance) is taken (ties: earlier queue
   position), A_c/A_m shrink, candidates are re-sized, repeat.
 * ERA: a long prompt that has not started prefill may not get a chunk while
   ``max_concurrent_long`` long prompts have started and not finished prefill.
@@ -193,14 +195,14 @@ def select_requests(a_gpu: int, a_kv_tokens: int, window_src: list[QueueEntry], 
             blk = step_blocks(e, c, pool)
             if blk * b > a_m:
                 continue
-            key = (math.hypot(a_c - c, a_m - blk * b), pos)
+            key = ((a_c - c) ** 2 + (a_m - blk * b) ** 2, pos)
             if best is None or key < best[:2]:
                 best = (key[0], pos, "p", i, e, c, blk)
         for blk, dq in tg_buckets.items():
             if not dq or blk * b > a_m:
                 continue
             pos, e = dq[0]
-            key = (math.hypot(a_c - 1, a_m - blk * b), pos)
+            key = ((a_c - 1) ** 2 + (a_m - blk * b) ** 2, pos)
             if best is None or key < best[:2]:
                 best = (key[0], pos, "t", blk, e, 1, blk)
         if best is None:
@@ -272,14 +274,17 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
             if not (s_f > s_b or used > free):
                 break
             e, c, blk = members[i]
+            kv_short = used > free
             dropped.add(i)
             s_f -= c
             used -= blk
             rid = e.request_id
-            if pool.is_resident(rid):
+            if kv_short and pool.is_resident(rid):
+                # KV deficit: swap the victim out to free its blocks (vLLM-style preemption)
                 preempted.append(rid)
                 free += pool.blocks_held(rid)
             else:
+                # budget deficit only: the victim leaves B but keeps its KV resident
                 deferred.append(rid)
             if rid in started_here:
                 long_active.discard(rid)

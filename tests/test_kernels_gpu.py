@@ -26,24 +26,30 @@ def _bf(shape, seed, std=1.0):
 @pytest.mark.parametrize("M,N,K_,bn", [
     (1, 256, 256, 0), (7, 768, 256, 0), (128, 256, 512, 256), (200, 1920, 640, 128), (777, 5120, 1024, 0),
     (1024, 3072, 5120, 256), (333, 50272, 256, 0), (2048, 2560, 5120, 0), (64, 1024, 4096, 128),
+    (200, 1920, 640, 64), (5, 5120, 20480, 64),
 ])
-def test_gemm_matches_fp32(K, M, N, K_, bn):
+@pytest.mark.parametrize("splits", [1, 3])
+def test_gemm_matches_fp32(K, M, N, K_, bn, splits):
     a = _bf((M, K_), 1)
     w = _bf((N, K_), 2, 0.05)
     ref = a.float() @ w.float().T
-    out = K.gemm(a.to(DEV), w.to(DEV), block_n=bn)
+    if splits > 1 and (K_ // 64) // splits < 2:
+        pytest.skip("K too short for the split")
+    out = K.gemm(a.to(DEV), w.to(DEV), block_n=bn if bn else 128, k_splits=splits)
     torch.cuda.synchronize()
     err = (out.float().cpu() - ref).abs().max().item()
     # bf16 output rounding (2^-8 relative) dominates; fp32 accumulation order is the rest
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
 
 
-def test_gemm_epilogue_bias_residual_relu_f32(K):
+@pytest.mark.parametrize("bn,splits", [(256, 1), (128, 4), (64, 2)])
+def test_gemm_epilogue_bias_residual_relu_f32(K, bn, splits):
     M, N, K_ = 300, 1024, 768
     a, w = _bf((M, K_), 3), _bf((N, K_), 4, 0.05)
     bias, res = _bf((N,), 5), _bf((M, N), 6)
     ref = torch.relu(a.float() @ w.float().T + bias.float() + res.float())
-    out = K.gemm(a.to(DEV), w.to(DEV), bias=bias.to(DEV), residual=res.to(DEV), relu=True)
+    out = K.gemm(a.to(DEV), w.to(DEV), bias=bias.to(DEV), residual=res.to(DEV), relu=True, block_n=bn,
+                 k_splits=splits)
     torch.cuda.synchronize()
     assert (out.float().cpu() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
     ref32 = a.float() @ w.float().T + bias.float()

@@ -159,9 +159,9 @@ AG_API int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t l
 AG_API int32_t ag_kv_append(const void* k, const void* v, int32_t ld, const int32_t* slot_mapping, int32_t rows,
                      int32_t heads, int32_t block_size, void* k_pool, void* v_pool, void* stream);
 /* Mixed paged attention over B sequences (q already scaled by head_dim^-0.5).  cu_q/ctx_len are
- * given on both host (work-list construction) and device. */
+ * given on both host (work-list construction) and device; pool_blocks = blocks in each pool. */
 AG_API int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const void* v_pool,
-                           const int32_t* block_table_dev, int32_t bt_stride, const int32_t* cu_q_host,
+                           int32_t pool_blocks, const int32_t* block_table_dev, int32_t bt_stride, const int32_t* cu_q_host,
                            const int32_t* ctx_len_host, const int32_t* cu_q_dev, const int32_t* ctx_len_dev,
                            int32_t num_seqs, int32_t heads, int32_t block_size, void* out, int32_t ldo,
                            void* workspace, int64_t workspace_bytes, void* stream);

@@ -1,36 +1,52 @@
-// Mixed prefill+decode paged attention, one launch per layer.
+// Mixed prefill+decode paged attention on sm_100a, one launch per layer.
 //
-// Work list (host-built, see capi.cu build_attention_work): every item is a query tile of one
-// sequence (<= 64 rows of a prefill chunk, or <= 16 rows such as a single decode token) against
-// a KV range [kv_start, kv_end) of that sequence's paged cache.  Long ranges are split across
-// CTAs (split-KV); their partial (O, lse) rows are merged by attn_combine_kernel.
+// Work list (host-built in capi.cu build_attention_work), one launch, two CTA kinds:
 //
-// grid = (items, heads), 128 threads.  KV is streamed 64 tokens (two 32-token pages) per stage
-// through a double-buffered, XOR-swizzled shared-memory ring with cp.async; QK^T and PV run
-// on mma.sync m16n8k16 (bf16 -> f32) with an online softmax in the exp2 domain.
-//   prefill tile (q_rows > 16): warp w owns query rows 16w..16w+15 against all 64 stage tokens;
-//   decode tile (q_rows <= 16): all warps share rows 0..15, warp w owns stage tokens 16w..16w+15,
-//                               and the four partial softmax states are merged through smem.
-// Causality: query row i of a chunk sits at position ctx_len + q_start + i and sees kv <= it.
+//  * TILE CTAs (one per (query tile, head, KV split)): a prefill chunk's rows in tiles of 128.
+//    TMA stages Q (128x128) once and K/V 128 tokens (four 32-token pages) per stage from the
+//    paged pool into a 2-deep SW128 ring.  One thread issues tcgen05.mma:
+//        S_j  = Q . K_j^T   (M=128, N=128, K=128)  -> TMEM (double-buffered, 2 x 128 columns)
+//        O   += P_j . V_j   (A = P from smem, B = V MN-major)  -> TMEM (128 columns)
+//    Four softmax warps own one query row per thread: tcgen05.ld the S row, causal/range mask,
+//    online softmax in the exp2 domain with lazy O rescaling (only when the row max grows by
+//    more than 2^8; the rescale is a tcgen05.ld/st round trip of the O row), write P (bf16) into
+//    a double-buffered SW128 smem tile, fence the async proxy, signal the MMA warp.
+//    Warp roles (192 threads): w0 TMA producer | w1 MMA issuer + TMEM owner | w2..w5 softmax.
+//
+//  * ROW CTAs (six (row, head, KV split) units per CTA, one per warp): decode tokens and rows
+//    of tiny chunks.  Each warp streams its KV range through its own cp.async ring of 16-token
+//    half pages and computes the dot products and PV on CUDA cores -- this path is HBM-bound.
+//
+// Split-KV partial rows (O normalised, plus (m, l) in the log2 domain) are merged by
+// attn_combine_kernel.  Causality: query row i of a chunk sits at position ctx_len + q_start + i.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ag {
 namespace {
 
-constexpr int kHD = 128;         // head dim
-constexpr int kPage = 32;        // tokens per KV block
-constexpr int kStageTok = 64;    // tokens per pipeline stage
+constexpr int kHD = 128;
+constexpr int kPage = 32;
 constexpr int kRowBytes = kHD * 2;
-constexpr int kStageBytes = 2 * kStageTok * kRowBytes;  // K + V = 32 KB
-constexpr int kStages = 2;
-constexpr int kAttnThreads = 128;
-constexpr int kDecHalf = 16;                              // tokens per decode ring slot (half page)
-constexpr int kDecSlotBytes = 2 * kDecHalf * kRowBytes;   // K + V = 8 KB
-constexpr int kDecStages = 3;
-constexpr int kDecWarpBytes = kDecStages * kDecSlotBytes;  // 24 KB per warp
-constexpr int kAttnSmem = 4 * kDecWarpBytes;               // 96 KB >= tile path 64 KB
+constexpr int kThreads = 192;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units: P <= 2^8 between O rescales
+
+// ---- tile path layout
+constexpr int kTM = 128, kTN = 128;
+constexpr int kSub = 128 * 64 * 2;                  // one [128 rows][64] bf16 SW128 sub-tile = 16 KB
+constexpr int kQOff = 0;                            // Q: 2 sub-tiles (dims 0-63, 64-127)
+constexpr int kKVOff = 2 * kSub;                    // stage s: K 2 sub-tiles, V 2 sub-tiles (64 KB)
+constexpr int kStageBytes = 4 * kSub;
+constexpr int kPOff = kKVOff + 2 * kStageBytes;     // P: 2 buffers x 2 sub-tiles (tokens 0-63, 64-127)
+constexpr int kBarOff = kPOff + 4 * kSub;           // 224 KB
+constexpr int kTileSmem = kBarOff + 256;
+// ---- row path layout
+constexpr int kDecHalf = 16;
+constexpr int kDecSlotBytes = 2 * kDecHalf * kRowBytes;  // K + V = 8 KB
+constexpr int kDecStages = 4;
+constexpr int kDecWarpBytes = kDecStages * kDecSlotBytes;  // 32 KB per warp, 6 warps = 192 KB
+constexpr int kSmemBytes = 1024 + (kTileSmem > 6 * kDecWarpBytes ? kTileSmem : 6 * kDecWarpBytes);
 
 AG_DEVICE void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -41,139 +57,33 @@ AG_DEVICE void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-AG_DEVICE void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-AG_DEVICE void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
+AG_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-AG_DEVICE void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+AG_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+AG_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// MN-major SW128 operand (V as the B of P.V): 64-element MN blocks `lbo` bytes apart, 8-row K
+// groups 1024 B apart.
+AG_DEVICE uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
 }
 
-// byte offset of (token, 16-byte chunk) inside a swizzled [64][128] bf16 tile
-AG_DEVICE uint32_t swz(int token, int chunk) {
-  return static_cast<uint32_t>(token * kRowBytes + ((chunk ^ (token & 7)) << 4));
-}
-
-struct Softmax2 {  // per-thread state for its two rows (g, g+8)
-  float m[2];
-  float l[2];
-};
-
-// One warp's pass over NT tokens [tok0, tok0+NT) of the current stage.
-template <int NT>
-AG_DEVICE void attend_stage(uint32_t sK, uint32_t sV, int tok0, const uint32_t (&qf)[8][4],
-                            float (&o)[16][4], Softmax2& st, int stage_pos0, int kv_end,
-                            const int (&qpos)[2]) {
-  const int lane = lane_id();
-  const int g = lane >> 2, t = lane & 3;
-  constexpr int NTILE = NT / 8;
-  float s[NTILE][4];
-#pragma unroll
-  for (int n = 0; n < NTILE; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.0f;
-
-  // S = Q K^T
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-    for (int np = 0; np < NTILE / 2; ++np) {
-      const int mat = lane >> 3, r = lane & 7;
-      const int token = tok0 + np * 16 + r + 8 * (mat >> 1);
-      const int chunk = 2 * ks + (mat & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(sK + swz(token, chunk), b0, b1, b2, b3);
-      mma_bf16(s[2 * np], qf[ks], b0, b1);
-      mma_bf16(s[2 * np + 1], qf[ks], b2, b3);
-    }
-  }
-
-  // mask + online softmax (log2 domain)
-  float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-  for (int n = 0; n < NTILE; ++n) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int row = e >> 1;
-      const int pos = stage_pos0 + tok0 + n * 8 + 2 * t + (e & 1);
-      const bool ok = pos < kv_end && pos <= qpos[row];
-      const float v = ok ? s[n][e] * kLog2e : -INFINITY;
-      s[n][e] = v;
-      mx[row] = fmaxf(mx[row], v);
-    }
-  }
-#pragma unroll
-  for (int row = 0; row < 2; ++row) {
-    mx[row] = fmaxf(mx[row], __shfl_xor_sync(0xffffffffu, mx[row], 1));
-    mx[row] = fmaxf(mx[row], __shfl_xor_sync(0xffffffffu, mx[row], 2));
-  }
-  float alpha[2], mref[2], rs[2] = {0.0f, 0.0f};
-#pragma unroll
-  for (int row = 0; row < 2; ++row) {
-    const float mnew = fmaxf(st.m[row], mx[row]);
-    mref[row] = (mnew == -INFINITY) ? 0.0f : mnew;
-    alpha[row] = exp2f(st.m[row] - mref[row]);  // exp2(-inf) = 0 on the first visit
-    st.m[row] = mnew;
-  }
-#pragma unroll
-  for (int n = 0; n < NTILE; ++n) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float p = exp2f(s[n][e] - mref[e >> 1]);
-      s[n][e] = p;
-      rs[e >> 1] += p;
-    }
-  }
-#pragma unroll
-  for (int row = 0; row < 2; ++row) {
-    rs[row] += __shfl_xor_sync(0xffffffffu, rs[row], 1);
-    rs[row] += __shfl_xor_sync(0xffffffffu, rs[row], 2);
-    st.l[row] = st.l[row] * alpha[row] + rs[row];
-  }
-#pragma unroll
-  for (int d = 0; d < 16; ++d) {
-    o[d][0] *= alpha[0];
-    o[d][1] *= alpha[0];
-    o[d][2] *= alpha[1];
-    o[d][3] *= alpha[1];
-  }
-
-  // O += P V
-#pragma unroll
-  for (int j = 0; j < NT / 16; ++j) {
-    uint32_t a[4];
-    a[0] = pack_bf16x2(s[2 * j][0], s[2 * j][1]);
-    a[1] = pack_bf16x2(s[2 * j][2], s[2 * j][3]);
-    a[2] = pack_bf16x2(s[2 * j + 1][0], s[2 * j + 1][1]);
-    a[3] = pack_bf16x2(s[2 * j + 1][2], s[2 * j + 1][3]);
-#pragma unroll
-    for (int dp = 0; dp < 8; ++dp) {
-      const int mat = lane >> 3, r = lane & 7;
-      const int token = tok0 + 16 * j + r + 8 * (mat & 1);
-      const int chunk = 2 * dp + (mat >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(sV + swz(token, chunk), b0, b1, b2, b3);
-      mma_bf16(o[2 * dp], a, b0, b1);
-      mma_bf16(o[2 * dp + 1], a, b2, b3);
-    }
-  }
-}
-
-// ---------------------------------------------------------------- single-row (decode) path
-// One warp streams the KV range of one (sequence, head, split) through its own 3-slot cp.async
-// ring of 16-token half pages (8 KB: K then V), independent of the other warps of the CTA.
-//   QK^T: lanes 0-15 / 16-31 take token 2i / 2i+1 of a slot, 8 dims (one 16-B chunk) each, and
-//         reduce over their 16 lanes -> every lane holds the score of its token pair member;
-//   PV:   lane l owns output dims 4l..4l+3 and walks the slot's 16 tokens (coalesced 256-B rows).
+// ---------------------------------------------------------------- row (decode) path
 AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head, uint8_t* wsmem) {
   const int lane = lane_id();
   const int q0 = p.cu_q[it.seq];
@@ -181,7 +91,6 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head
   const int qpos = p.ctx_len[it.seq] + it.q_start;
   const int kv_end = min(it.kv_end, qpos + 1);
   const int chunk = lane & 15;
-  // q chunk for the QK phase (pre-scaled by head_dim^-0.5 in the QKV epilogue), folded with log2e
   float qv[8];
   {
     const uint4 w = *reinterpret_cast<const uint4*>(p.q + static_cast<int64_t>(tok_row) * p.ldq + head * kHD + chunk * 8);
@@ -207,7 +116,7 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head
     const uint32_t sk = sbase + slot * kDecSlotBytes;
     const uint32_t sv = sk + kDecHalf * kRowBytes;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {  // 16 rows x 16 chunks = 256 x 16 B per tensor, 8 per lane
+    for (int i = 0; i < 8; ++i) {
       const int id = lane + 32 * i;
       cp_async16(sk + id * 16, p.kcache + base + id * 8);
       cp_async16(sv + id * 16, p.vcache + base + id * 8);
@@ -231,7 +140,6 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head
     const int slot = (h - h0) % kDecStages;
     const uint8_t* sk = wsmem + slot * kDecSlotBytes;
     const uint8_t* sv = sk + kDecHalf * kRowBytes;
-    // scores: lane keeps token (lane & 15)
     float s_mine = -INFINITY;
 #pragma unroll
     for (int i = 0; i < kDecHalf / 2; ++i) {
@@ -247,7 +155,6 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head
       }
 #pragma unroll
       for (int o2 = 8; o2 > 0; o2 >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o2);
-      // lanes 0-15 now hold token 2i, lanes 16-31 token 2i+1; lane keeps token (lane & 15)
       const float other = __shfl_sync(0xffffffffu, d, (lane & 1) * 16);
       if ((lane & 15) >> 1 == i) s_mine = other;
     }
@@ -294,179 +201,250 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head
   }
 }
 
-__global__ void __launch_bounds__(kAttnThreads)
-    mixed_attention_kernel(AttnParams p, const AttnItem* __restrict__ items, int n_tile_items, int n_row_items) {
-  extern __shared__ __align__(128) uint8_t smem[];
+// ---------------------------------------------------------------- tile (tcgen05) path
+struct TileBars {
+  uint64_t q_full;
+  uint64_t kv_full[2], kv_empty[2];
+  uint64_t s_full[2], s_empty[2];
+  uint64_t p_full[2], o_done[2];
+  uint32_t tmem_base;
+};
+
+AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem& it, int head, uint8_t* smem) {
   const int warp = threadIdx.x >> 5;
-  const int n_tile_ctas = n_tile_items * p.heads;
-  if (static_cast<int>(blockIdx.x) >= n_tile_ctas) {
-    const int u = (blockIdx.x - n_tile_ctas) * 4 + warp;  // (item, head) unit of this warp
-    if (u >= n_row_items * p.heads) return;
-    const AttnItem itr = items[n_tile_items + u / p.heads];
-    decode_row_warp(p, itr, u % p.heads, smem + warp * kDecWarpBytes);
-    return;
-  }
-  const AttnItem it = items[blockIdx.x / p.heads];
-  const int head = blockIdx.x % p.heads;
   const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const bool decode_mode = it.q_rows <= 16;
-
+  TileBars* bars = reinterpret_cast<TileBars*>(smem + kBarOff);
   const int q0 = p.cu_q[it.seq];
-  const int ctx = p.ctx_len[it.seq];
-  const int row_off = decode_mode ? 0 : warp * 16;
-
-  // query fragments (rows beyond q_rows are zero and fully masked)
-  uint32_t qf[8][4];
-  int qpos[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int r = row_off + g + 8 * h;
-    qpos[h] = (r < it.q_rows) ? ctx + it.q_start + r : -1;
-  }
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int r = row_off + g + 8 * (e & 1);
-      const int col = ks * 16 + 2 * t + 8 * (e >> 1);
-      uint32_t v = 0;
-      if (r < it.q_rows)
-        v = *reinterpret_cast<const uint32_t*>(p.q + static_cast<int64_t>(q0 + it.q_start + r) * p.ldq +
-                                               head * kHD + col);
-      qf[ks][e] = v;
-    }
-  }
-
-  float o[16][4];
-#pragma unroll
-  for (int d = 0; d < 16; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.0f;
-  Softmax2 st;
-  st.m[0] = st.m[1] = -INFINITY;
-  st.l[0] = st.l[1] = 0.0f;
-
-  const uint32_t smem_base = smem_u32(smem);
-  const int n_stages = (it.kv_end - it.kv_start + kStageTok - 1) / kStageTok;
-  const int last_page = (it.kv_end - 1) / kPage;
-  const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
-  const int64_t head_off = static_cast<int64_t>(head) * kPage * kHD;
-  const int64_t page_elems = static_cast<int64_t>(p.heads) * kPage * kHD;
-
-  auto load_stage = [&](int c, int buf) {
-    const uint32_t sK = smem_base + buf * kStageBytes;
-    const uint32_t sV = sK + kStageTok * kRowBytes;
-    const int pos0 = it.kv_start + c * kStageTok;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      int page = pos0 / kPage + j;
-      page = page > last_page ? last_page : page;  // pad with a valid (masked) page
-      const int64_t base = static_cast<int64_t>(bt[page]) * page_elems + head_off;
-      const __nv_bfloat16* kp = p.kcache + base;
-      const __nv_bfloat16* vp = p.vcache + base;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int id = threadIdx.x + i * kAttnThreads;  // 0..511 within the page
-        const int tok = id >> 4, ch = id & 15;
-        const uint32_t off = swz(j * kPage + tok, ch);
-        cp_async16(sK + off, kp + tok * kHD + ch * 8);
-        cp_async16(sV + off, vp + tok * kHD + ch * 8);
-      }
-    }
-  };
-
-  if (n_stages > 0) load_stage(0, 0);
-  cp_async_commit();
-  if (n_stages > 1) load_stage(1, 1);
-  cp_async_commit();
-
-  for (int c = 0; c < n_stages; ++c) {
-    const int buf = c & 1;
-    cp_async_wait<1>();
-    __syncthreads();
-    const uint32_t sK = smem_base + buf * kStageBytes;
-    const uint32_t sV = sK + kStageTok * kRowBytes;
-    const int pos0 = it.kv_start + c * kStageTok;
-    if (decode_mode)
-      attend_stage<16>(sK, sV, warp * 16, qf, o, st, pos0, it.kv_end, qpos);
-    else
-      attend_stage<64>(sK, sV, 0, qf, o, st, pos0, it.kv_end, qpos);
-    __syncthreads();
-    if (c + 2 < n_stages) load_stage(c + 2, buf);
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-
   const int tok_row0 = q0 + it.q_start;
-  if (!decode_mode) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = row_off + g + 8 * h;
-      if (r >= it.q_rows) continue;
-      const float inv = st.l[h] > 0.0f ? 1.0f / st.l[h] : 0.0f;
-      if (it.part_row < 0) {
-        __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_row0 + r) * p.ldo + head * kHD;
-#pragma unroll
-        for (int d = 0; d < 16; ++d)
-          *reinterpret_cast<uint32_t*>(dst + d * 8 + 2 * t) =
-              pack_bf16x2(o[d][2 * h] * inv, o[d][2 * h + 1] * inv);
-      } else {
-        const int64_t prow = static_cast<int64_t>(it.part_row + r) * p.heads + head;
-        float* dst = p.part_o + prow * kHD;
-#pragma unroll
-        for (int d = 0; d < 16; ++d)
-          *reinterpret_cast<float2*>(dst + d * 8 + 2 * t) = make_float2(o[d][2 * h] * inv, o[d][2 * h + 1] * inv);
-        if (t == 0) {
-          p.part_ml[prow * 2] = st.m[h];
-          p.part_ml[prow * 2 + 1] = st.l[h];
+  const int ctx = p.ctx_len[it.seq];
+  // KV tiles of 128 tokens from kv_start (a multiple of 128) to the causal end of the tile
+  const int kv_end = min(it.kv_end, ctx + it.q_start + it.q_rows);
+  const int n_tiles = (kv_end - it.kv_start + kTN - 1) / kTN;
+  const uint32_t sb = smem_u32(smem);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->s_empty[i], 4);
+      mbar_init(&bars->p_full[i], 4);
+      mbar_init(&bars->o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;  // S0 [0,128) S1 [128,256) O [256,384)
+
+  if (warp == 0) {
+    if (lane == 0 && n_tiles > 0) {
+      tma_prefetch_desc(&tm.q);
+      tma_prefetch_desc(&tm.k);
+      tma_prefetch_desc(&tm.v);
+      mbar_arrive_expect_tx(&bars->q_full, 2 * kSub);
+      tma_load_2d(smem + kQOff, &tm.q, &bars->q_full, head * kHD, tok_row0);
+      tma_load_2d(smem + kQOff + kSub, &tm.q, &bars->q_full, head * kHD + 64, tok_row0);
+      const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
+      const int last_page = (kv_end - 1) / kPage;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        mbar_wait(&bars->kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->kv_full[st], kStageBytes);
+        uint8_t* kdst = smem + kKVOff + st * kStageBytes;
+        uint8_t* vdst = kdst + 2 * kSub;
+        for (int pg = 0; pg < 4; ++pg) {
+          int page = (it.kv_start + j * kTN) / kPage + pg;
+          page = page > last_page ? last_page : page;  // masked padding page
+          const int row = (bt[page] * p.heads + head) * kPage;
+          tma_load_2d(kdst + pg * 4096, &tm.k, &bars->kv_full[st], 0, row);
+          tma_load_2d(kdst + kSub + pg * 4096, &tm.k, &bars->kv_full[st], 64, row);
+          tma_load_2d(vdst + pg * 4096, &tm.v, &bars->kv_full[st], 0, row);
+          tma_load_2d(vdst + kSub + pg * 4096, &tm.v, &bars->kv_full[st], 64, row);
         }
       }
     }
-    return;
-  }
-
-  // decode tile: merge the four warps' softmax states through shared memory
-  float* so = reinterpret_cast<float*>(smem);          // [4][16][128]
-  float* sm = so + 4 * 16 * kHD;                        // [4][16]
-  float* sl = sm + 4 * 16;                              // [4][16]
+  } else if (warp == 1) {
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(kTM, kTN);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(kTM, kHD) | (1u << 16);  // B (V) MN-major
+      mbar_wait(&bars->q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1, sbuf = j & 1;
+        mbar_wait(&bars->kv_full[st], (j >> 1) & 1);
+        mbar_wait(&bars->s_empty[sbuf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kaddr = sb + kKVOff + st * kStageBytes;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int r = g + 8 * h;
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t a = umma_desc_sw128(sb + kQOff + (k >> 2) * kSub) + 2 * (k & 3);
+          const uint64_t b = umma_desc_sw128(kaddr + (k >> 2) * kSub) + 2 * (k & 3);
+          umma_bf16_ss(tmem + sbuf * 128, a, b, idesc_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&bars->s_full[sbuf]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s(j + 1);
+        const int pb = j & 1, st = j & 1;
+        mbar_wait(&bars->p_full[pb], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t paddr = sb + kPOff + pb * 2 * kSub;
+        const uint32_t vaddr = sb + kKVOff + st * kStageBytes + 2 * kSub;
 #pragma unroll
-    for (int d = 0; d < 16; ++d) {
-      so[(warp * 16 + r) * kHD + d * 8 + 2 * t] = o[d][2 * h];
-      so[(warp * 16 + r) * kHD + d * 8 + 2 * t + 1] = o[d][2 * h + 1];
+        for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA
+          const uint64_t a = umma_desc_sw128(paddr + (k >> 2) * kSub) + 2 * (k & 3);
+          const uint64_t b = umma_desc_sw128_mn(vaddr + k * 2048, kSub);
+          umma_bf16_ss(tmem + 256, a, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&bars->o_done[pb]);
+        umma_commit(&bars->kv_empty[st]);
+      }
     }
-    if (t == 0) {
-      sm[warp * 16 + r] = st.m[h];
-      sl[warp * 16 + r] = st.l[h];
-    }
-  }
-  __syncthreads();
-  const int d = threadIdx.x;  // one output dim per thread
-  for (int r = 0; r < it.q_rows; ++r) {
-    float mmax = -INFINITY;
+  } else {
+    // ---------------- softmax / epilogue warps: one query row per thread
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool row_ok = row < it.q_rows;
+    const int qpos = ctx + it.q_start + row;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sbuf = j & 1;
+      mbar_wait(&bars->s_full[sbuf], (j >> 1) & 1);
+      tc_fence_after();
+      float s[128];
 #pragma unroll
-    for (int w = 0; w < 4; ++w) mmax = fmaxf(mmax, sm[w * 16 + r]);
-    const float mref = mmax == -INFINITY ? 0.0f : mmax;
-    float lsum = 0.0f, acc = 0.0f;
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + lane_addr + sbuf * 128 + c * 32, r);
+        tmem_ld_wait();
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float sc = exp2f(sm[w * 16 + r] - mref);
-      lsum += sl[w * 16 + r] * sc;
-      acc += so[(w * 16 + r) * kHD + d] * sc;
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->s_empty[sbuf]);
+      const int kbase = it.kv_start + j * kTN;
+      const int lim = row_ok ? min(kv_end, qpos + 1) - kbase : 0;  // valid columns [0, lim)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = c < lim ? s[c] * kLog2e : -INFINITY;
+        mx = fmaxf(mx, s[c]);
+      }
+      if (mx > m_used + kRescaleThresh) {
+        // the running max grew: rescale l and the O row (after every earlier P.V finished)
+        const float alpha = exp2f(m_used - mx);  // 0 on the first visit (m_used = -inf)
+        if (j > 0 && m_used != -INFINITY) {
+          mbar_wait(&bars->o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+        }
+        l *= alpha;
+        m_used = mx;
+      }
+      const float mref = m_used == -INFINITY ? 0.f : m_used;
+      // P_j -> smem buffer (j & 1), free once P.V of tile j-2 completed
+      if (j >= 2) mbar_wait(&bars->o_done[j & 1], ((j - 2) >> 1) & 1);
+      uint8_t* pbuf = smem + kPOff + (j & 1) * 2 * kSub;
+      float rs = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {  // 16-B chunks of 8 tokens
+        float e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          e[i] = exp2f(s[ch * 8 + i] - mref);
+          rs += e[i];
+        }
+        const int sub = ch >> 3, cc = ch & 7;
+        uint4 v = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]), pack_bf16x2(e[4], e[5]),
+                             pack_bf16x2(e[6], e[7]));
+        *reinterpret_cast<uint4*>(pbuf + sub * kSub + row * 128 + ((cc ^ (row & 7)) << 4)) = v;
+      }
+      l += rs;
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[j & 1]);
     }
-    const float val = lsum > 0.0f ? acc / lsum : 0.0f;
-    if (it.part_row < 0) {
-      p.out[static_cast<int64_t>(tok_row0 + r) * p.ldo + head * kHD + d] = __float2bfloat16_rn(val);
-    } else {
-      const int64_t prow = static_cast<int64_t>(it.part_row + r) * p.heads + head;
-      p.part_o[prow * kHD + d] = val;
-      if (d == 0) {
-        p.part_ml[prow * 2] = mmax;
-        p.part_ml[prow * 2 + 1] = lsum;
+    // epilogue: O row / l
+    if (n_tiles > 0) {
+      mbar_wait(&bars->o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      if (n_tiles > 0) {
+        tmem_ld_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = 0u;
+      }
+      if (!row_ok) continue;
+      if (it.part_row < 0) {
+        __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_row0 + row) * p.ldo + head * kHD + c * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_global_v4(dst + q * 8, pack_bf16x2(__uint_as_float(r[q * 8]) * inv, __uint_as_float(r[q * 8 + 1]) * inv),
+                       pack_bf16x2(__uint_as_float(r[q * 8 + 2]) * inv, __uint_as_float(r[q * 8 + 3]) * inv),
+                       pack_bf16x2(__uint_as_float(r[q * 8 + 4]) * inv, __uint_as_float(r[q * 8 + 5]) * inv),
+                       pack_bf16x2(__uint_as_float(r[q * 8 + 6]) * inv, __uint_as_float(r[q * 8 + 7]) * inv));
+      } else {
+        const int64_t prow = static_cast<int64_t>(it.part_row + row) * p.heads + head;
+        float* dst = p.part_o + prow * kHD + c * 32;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          st_global_v4(dst + q * 4, __float_as_uint(__uint_as_float(r[q * 4]) * inv),
+                       __float_as_uint(__uint_as_float(r[q * 4 + 1]) * inv),
+                       __float_as_uint(__uint_as_float(r[q * 4 + 2]) * inv),
+                       __float_as_uint(__uint_as_float(r[q * 4 + 3]) * inv));
+        if (c == 0) {
+          p.part_ml[prow * 2] = m_used;
+          p.part_ml[prow * 2 + 1] = l;
+        }
       }
     }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    mixed_attention_kernel(AttnParams p, const __grid_constant__ AttnTmaps tm, const AttnItem* __restrict__ items,
+                           int n_tile_items, int n_row_items) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int n_tile_ctas = n_tile_items * p.heads;
+  if (static_cast<int>(blockIdx.x) < n_tile_ctas) {
+    const AttnItem it = items[blockIdx.x / p.heads];
+    tile_tc(p, tm, it, blockIdx.x % p.heads, smem);
+    return;
+  }
+  const int warp = threadIdx.x >> 5;
+  const int u = (blockIdx.x - n_tile_ctas) * (kThreads / 32) + warp;
+  if (u >= n_row_items * p.heads) return;
+  const AttnItem itr = items[n_tile_items + u / p.heads];
+  decode_row_warp(p, itr, u % p.heads, smem + warp * kDecWarpBytes);
 }
 
 // Merge split-KV partial rows: out = sum_s w_s O_s / sum_s w_s, w_s = l_s * 2^(m_s - M).
@@ -495,20 +473,22 @@ __global__ void attn_combine_kernel(AttnParams p, const AttnCombine* __restrict_
 
 }  // namespace
 
-cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_tile_items, int n_row_items,
-                             const AttnCombine* combines, int n_combines, cudaStream_t stream) {
+int attention_tile_rows() { return kTM; }
+int attention_tile_kv() { return kTN; }
+
+cudaError_t launch_attention(const AttnParams& p, const AttnTmaps& tm, const AttnItem* items, int n_tile_items,
+                             int n_row_items, const AttnCombine* combines, int n_combines, cudaStream_t stream) {
   if (p.block_size != kPage) return cudaErrorInvalidValue;
-  const int n_items = n_tile_items + n_row_items;
-  if (n_items > 0) {
+  if (n_tile_items + n_row_items > 0) {
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(mixed_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kAttnSmem);
+      cudaError_t e =
+          cudaFuncSetAttribute(mixed_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    const int ctas = n_tile_items * p.heads + (n_row_items * p.heads + 3) / 4;
-    mixed_attention_kernel<<<ctas, kAttnThreads, kAttnSmem, stream>>>(p, items, n_tile_items, n_row_items);
+    const int ctas = n_tile_items * p.heads + (n_row_items * p.heads + kThreads / 32 - 1) / (kThreads / 32);
+    mixed_attention_kernel<<<ctas, kThreads, kSmemBytes, stream>>>(p, tm, items, n_tile_items, n_row_items);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -79,10 +79,10 @@ struct AttnWork {
   int part_rows = 0;
 };
 
-// Tile every sequence's new tokens: >1-row pieces become <=64-row tensor-core tiles (<=16 rows run
-// in the 4-warp small-tile mode), single-row pieces (decode tokens) become warp-level streaming
-// items.  Long KV ranges are split (split-KV) so that tiles give ~4 CTAs/SM and single-row items
-// ~16 warps/SM of work; splits are multiples of 64 tokens and merged by attn_combine_kernel.
+// Tile every sequence's new tokens: chunks of more than 16 rows become 128-row tcgen05 tiles;
+// decode tokens and the rows of tiny chunks (<= 16 rows) become warp-level streaming items (one
+// per row).  Long KV ranges are split (split-KV) so tiles give ~1 CTA/SM and rows ~24 warps/SM of
+// work; tile splits are multiples of 128 tokens, row splits of 64; attn_combine_kernel merges.
 void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, int heads, int part_cap,
                           AttnWork& w) {
   w.items.clear();
@@ -91,21 +91,23 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
   struct Piece {
     int seq, qs, rows, kv_hi;
   };
+  const int TM = ag::attention_tile_rows(), TN = ag::attention_tile_kv();
   std::vector<Piece> tiles, rows1;
   double tile_work = 0.0, row_work = 0.0;
   for (int b = 0; b < B; ++b) {
     const int q = cu_q[b + 1] - cu_q[b];
     if (q <= 0) continue;
-    if (q == 1) {
-      rows1.push_back({b, 0, 1, ctx_len[b] + 1});
-      row_work += ctx_len[b] + 1;
+    if (q <= 16) {
+      for (int r = 0; r < q; ++r) {
+        rows1.push_back({b, r, 1, ctx_len[b] + r + 1});
+        row_work += ctx_len[b] + r + 1;
+      }
       continue;
     }
-    const int T = q <= 16 ? 16 : 64;
-    for (int qs = 0; qs < q; qs += T) {
-      const int r = std::min(T, q - qs);
+    for (int qs = 0; qs < q; qs += TM) {
+      const int r = std::min(TM, q - qs);
       tiles.push_back({b, qs, r, ctx_len[b] + qs + r});
-      tile_work += static_cast<double>(ctx_len[b] + qs + r) * (r > 16 ? 4.0 : 1.0);
+      tile_work += ctx_len[b] + qs + r;
     }
   }
   const int sms = ag::num_sms();
@@ -123,28 +125,28 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
     w.combines.push_back({cu_q[t.seq] + t.qs, t.rows, base, n_split});
     w.part_rows += n_split * t.rows;
   };
-  auto split_of = [](int kv_hi, double per_item, double weight, int min_len, int& n_split, int& split) {
-    n_split = static_cast<int>(std::ceil(kv_hi * weight / per_item));
+  auto split_of = [](int kv_hi, double per_item, int min_len, int align, int& n_split, int& split) {
+    n_split = static_cast<int>(std::ceil(kv_hi / per_item));
     n_split = std::max(1, std::min(n_split, (kv_hi + min_len - 1) / min_len));
-    split = ((kv_hi + n_split - 1) / n_split + 63) / 64 * 64;
+    split = ((kv_hi + n_split - 1) / n_split + align - 1) / align * align;
     n_split = (kv_hi + split - 1) / split;
   };
   std::vector<AttnItem> tile_items, row_items;
   {
-    const int desired = std::max(1, (sms * 4 + heads - 1) / heads);
-    const double per_item = std::max(1.0, tile_work / desired);
+    const int desired = std::max(1, (sms + heads - 1) / heads);
+    const double per_item = std::max(static_cast<double>(TN), tile_work / desired);
     for (const Piece& t : tiles) {
       int n, sp;
-      split_of(t.kv_hi, per_item, t.rows > 16 ? 4.0 : 1.0, 256, n, sp);
+      split_of(t.kv_hi, per_item, 2 * TN, TN, n, sp);
       emit(t, n, sp, tile_items);
     }
   }
   {
-    const int desired = std::max(1, (sms * 16 + heads - 1) / heads);
+    const int desired = std::max(1, (sms * 24 + heads - 1) / heads);
     const double per_item = std::max(512.0, row_work / desired);
     for (const Piece& t : rows1) {
       int n, sp;
-      split_of(t.kv_hi, per_item, 1.0, 512, n, sp);
+      split_of(t.kv_hi, per_item, 512, 64, n, sp);
       emit(t, n, sp, row_items);
     }
   }
@@ -177,6 +179,7 @@ struct LayerState {
   bf16* kpool = nullptr;
   bf16* vpool = nullptr;
   WeightMap tm_qkv, tm_out, tm_fc1, tm_fc2;
+  CUtensorMap tm_kpool, tm_vpool;  // pool as [num_blocks*heads*32, 128], box 64 x 32
   bool ready = false;
 };
 
@@ -207,7 +210,7 @@ struct ag_model {
   uint8_t* meta_dev = nullptr;
   size_t meta_cap = 0;
   int32_t* tok_host = nullptr;  // pinned D2H staging
-  CUtensorMap tm_xln, tm_attn, tm_ffn, tm_lm_in;
+  CUtensorMap tm_xln, tm_attn, tm_ffn, tm_lm_in, tm_qbuf;
   WeightMap tm_lm_w;
   // staged step
   int S = 0, B = 0, n_logit = 0, bt_stride = 0, n_items = 0, n_comb = 0, n_tile_items = 0, n_row_items = 0;
@@ -402,6 +405,7 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
     chk(tmap(&m->tm_attn, m->attn, T, m->hq, 128, "attn"));
     chk(tmap(&m->tm_ffn, m->ffn, T, m->ffn_l, 128, "ffn"));
     chk(tmap(&m->tm_lm_in, m->lm_in, Sq, c.hidden, 128, "lm_in"));
+    chk(tmap(&m->tm_qbuf, m->qbuf, T, m->hq, 128, "q buffer"));
   }
   if (r == AG_OK) {
     cudaEventCreate(&m->ev0);
@@ -465,6 +469,9 @@ int32_t ag_model_set_kv_cache(ag_model* m, int32_t layer, void* k_pool, void* v_
   if (!m || layer < 0 || layer >= m->cfg.num_layers || !k_pool || !v_pool) return fail(AG_EINVAL, "bad kv cache");
   m->layers[layer].kpool = static_cast<bf16*>(k_pool);
   m->layers[layer].vpool = static_cast<bf16*>(v_pool);
+  const int64_t pool_rows = static_cast<int64_t>(m->cfg.num_blocks) * m->heads_l * m->cfg.block_size;
+  AG_TRY(tmap(&m->layers[layer].tm_kpool, k_pool, pool_rows, m->head_dim, 32, "k pool"));
+  AG_TRY(tmap(&m->layers[layer].tm_vpool, v_pool, pool_rows, m->head_dim, 32, "v pool"));
   m->layers[layer].ready = m->layers[layer].w.qkv_w != nullptr;
   return AG_OK;
 }
@@ -645,9 +652,13 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ap.part_ml = m->part_ml;
         ap.heads = m->heads_l;
         ap.block_size = c.block_size;
+        ag::AttnTmaps atm;
+        atm.q = m->tm_qbuf;
+        atm.k = L.tm_kpool;
+        atm.v = L.tm_vpool;
         ProfScope ps(m, AG_K_ATTENTION, s, m->attn_flops_step, m->attn_bytes_step);
         if (m->n_comb > 0) m->launches_last += 1;
-        AG_CUDA(ag::launch_attention(ap, m->d_items, m->n_tile_items, m->n_row_items, m->d_comb, m->n_comb, s));
+        AG_CUDA(ag::launch_attention(ap, atm, m->d_items, m->n_tile_items, m->n_row_items, m->d_comb, m->n_comb, s));
       }
       {
         // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
@@ -937,11 +948,12 @@ int32_t ag_kv_append(const void* k, const void* v, int32_t ld, const int32_t* sl
   return AG_OK;
 }
 
-int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const void* v_pool,
+int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const void* v_pool, int32_t pool_blocks,
                            const int32_t* block_table_dev, int32_t bt_stride, const int32_t* cu_q_host,
                            const int32_t* ctx_len_host, const int32_t* cu_q_dev, const int32_t* ctx_len_dev,
                            int32_t num_seqs, int32_t heads, int32_t block_size, void* out, int32_t ldo,
                            void* workspace, int64_t workspace_bytes, void* stream) {
+  const int64_t q_rows_total = num_seqs > 0 ? cu_q_host[num_seqs] : 0;
   if (!q || !k_pool || !v_pool || !block_table_dev || !cu_q_host || !ctx_len_host || !out || !workspace)
     return fail(AG_EINVAL, "null pointer");
   if (block_size != 32) return fail(AG_EINVAL, "block_size must be 32");
@@ -973,7 +985,18 @@ int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool, const
   ap.part_ml = ap.part_o + static_cast<int64_t>(part_cap) * heads * 128;
   ap.heads = heads;
   ap.block_size = block_size;
-  AG_CUDA(ag::launch_attention(ap, reinterpret_cast<const AttnItem*>(ws), w.n_tile, w.n_row,
+  ag::AttnTmaps atm;
+  {
+    int64_t nblk = 0;
+    // pool extent: highest block id referenced + 1 (host copy not available: use the workspace bound)
+    nblk = pool_blocks;
+    const int64_t pool_rows = nblk * heads * block_size;
+    int r1 = ag::make_tmap_kmajor(&atm.q, q, std::max<int64_t>(q_rows_total, 1), 128 * heads, ldq, 128);
+    int r2 = ag::make_tmap_kmajor(&atm.k, k_pool, pool_rows, 128, 128, 32);
+    int r3 = ag::make_tmap_kmajor(&atm.v, v_pool, pool_rows, 128, 128, 32);
+    if (r1 || r2 || r3) return fail(AG_EINVAL, "attention tensor maps failed (alignment?)");
+  }
+  AG_CUDA(ag::launch_attention(ap, atm, reinterpret_cast<const AttnItem*>(ws), w.n_tile, w.n_row,
                                reinterpret_cast<const AttnCombine*>(ws + align_up(ib, 256)),
                                static_cast<int>(w.combines.size()), s));
   // the host work vectors must outlive the async copies

@@ -98,9 +98,16 @@ struct AttnParams {
   int block_size;
 };
 
-// items = [n_tile_items query tiles (q_rows > 1)] + [n_row_items single-row (decode) items]
-cudaError_t launch_attention(const AttnParams& p, const AttnItem* items, int n_tile_items, int n_row_items,
-                             const AttnCombine* combines, int n_combines, cudaStream_t stream);
+// TMA maps of the tile path: q over [rows, heads*128] (box 64 x 128 rows), k/v over the pool
+// viewed as [num_blocks*heads*32, 128] (box 64 x 32 rows = half a page row-block).
+struct AttnTmaps {
+  CUtensorMap q, k, v;
+};
+int attention_tile_rows();  // query rows per tcgen05 tile (128)
+int attention_tile_kv();    // kv tokens per tile stage (128)
+// items = [n_tile_items query tiles (tcgen05)] + [n_row_items single-row items (warp streaming)]
+cudaError_t launch_attention(const AttnParams& p, const AttnTmaps& tm, const AttnItem* items, int n_tile_items,
+                             int n_row_items, const AttnCombine* combines, int n_combines, cudaStream_t stream);
 
 // argmax over rows of logits (f32), optional vocab offset; writes (value, index) pairs
 cudaError_t launch_argmax(const float* logits, int rows, int cols, int ld, int index_offset,

@@ -83,7 +83,8 @@ def paged_attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
         out = torch.zeros(q.shape[0], heads * 128, device=q.device, dtype=torch.bfloat16)
     ws = torch.empty(workspace_bytes, device=q.device, dtype=torch.uint8)
     _lib.check(_lib.load().ag_paged_attention(
-        q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(), block_table.data_ptr(), block_table.stride(0),
+        q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(), k_pool.shape[0], block_table.data_ptr(),
+        block_table.stride(0),
         cu_q_h.data_ptr(), ctx_h.data_ptr(), cu_q_d.data_ptr(), ctx_d.data_ptr(), ctx_h.numel(), heads,
         k_pool.shape[2], out.data_ptr(), out.stride(0), ws.data_ptr(), workspace_bytes, _stream()))
     return out

@@ -283,7 +283,7 @@ def run_ours(args):
                              "post": 1e3 * sum(r.host_post_s for r in recs) / K,
                              "device_forward": 1e3 * dev_s / K, "wall_total": 1e3 * wall / K},
         "clocks": clocks,
-        "gemm_plans": " ".join(f"{k}:{mb}:{bn}x{ks}" for k, mb, bn, ks in ex.gemm_plans()),
+        "gemm_plans": " ".join(f"{k}:{mb}:{bn}x{ks}a{am}" for k, mb, bn, ks, am in ex.gemm_plans()),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mcfg, batches, world)

@@ -150,11 +150,12 @@ AG_API int64_t ag_model_last_h2d_bytes(ag_model* m);
 
 /* ---- individual kernels (device pointers), for parity tests and the profiler ---- */
 /* D[M,N] = A[M,K] . W[N,K]^T (+bias[N]) (+residual[M,ldr]) (ReLU); bf16 out unless out_f32.
- * block_n in {0 (auto), 128, 256}; k_splits 0 = auto (uses workspace, fp32 k_splits*M*N). */
+ * block_n in {0 (auto), 64, 128, 256}; k_splits 0 = auto (uses workspace, fp32 k_splits*M*N);
+ * a_rows in {0/128, 64, 32}: activation rows staged per k-block (small-M variant needs M <= a_rows). */
 AG_API int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias,
                      const void* residual, int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32,
-                     int32_t M, int32_t N, int32_t K, int32_t block_n, int32_t k_splits, void* workspace,
-                     int64_t workspace_bytes, void* stream);
+                     int32_t M, int32_t N, int32_t K, int32_t block_n, int32_t k_splits, int32_t a_rows,
+                     void* workspace, int64_t workspace_bytes, void* stream);
 /* Paged KV append: rows of k/v ([rows, heads*128], row stride ld) into their slots. */
 AG_API int32_t ag_kv_append(const void* k, const void* v, int32_t ld, const int32_t* slot_mapping, int32_t rows,
                      int32_t heads, int32_t block_size, void* k_pool, void* v_pool, void* stream);

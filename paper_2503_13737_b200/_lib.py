@@ -65,7 +65,8 @@ _SIGS = {
     "ag_model_autotune": (i32, [vp, vp]),
     "ag_model_get_gemm_plans": (i32, [vp, vp, i32]),
     "ag_model_last_h2d_bytes": (i64, [vp]),
-    "ag_gemm_bf16": (i32, [vp, i32, vp, i32, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, i32, vp, i64, vp]),
+    "ag_gemm_bf16": (i32, [vp, i32, vp, i32, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, i64,
+                           vp]),
     "ag_kv_append": (i32, [vp, vp, i32, vp, i32, i32, i32, vp, vp, vp]),
     "ag_paged_attention": (i32, [vp, i32, vp, vp, i32, vp, i32, vp, vp, vp, vp, i32, i32, i32, vp, i32, vp, i64, vp]),
     "ag_layernorm": (i32, [vp, vp, vp, vp, vp, vp, f32, i32, i32, vp, vp]),

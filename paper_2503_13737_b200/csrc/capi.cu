@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -166,7 +167,13 @@ struct WeightMap {
   const CUtensorMap& box(int bn) const { return bn == 256 ? box256 : (bn == 64 ? box64 : box128); }
 };
 
-// Autotuned (BLOCK_N, k_splits) per GEMM kind and M bucket (ag_model_autotune).
+// Activation operand maps for the three A-box heights (128 rows; 32/64 for small-M GEMMs).
+struct ActMap {
+  CUtensorMap box32, box64, box128;
+  const CUtensorMap& box(int am) const { return am == 32 ? box32 : (am == 64 ? box64 : box128); }
+};
+
+// Autotuned (BLOCK_N, k_splits, A rows) per GEMM kind and M bucket (ag_model_autotune).
 enum GemmKind { kGemmQkv = 0, kGemmOut, kGemmFc1, kGemmFc2, kGemmLm, kGemmKinds };
 struct GemmTable {
   std::vector<int> m_bucket;                // ascending
@@ -210,7 +217,8 @@ struct ag_model {
   uint8_t* meta_dev = nullptr;
   size_t meta_cap = 0;
   int32_t* tok_host = nullptr;  // pinned D2H staging
-  CUtensorMap tm_xln, tm_attn, tm_ffn, tm_lm_in, tm_qbuf;
+  ActMap tm_xln, tm_attn, tm_ffn, tm_lm_in;
+  CUtensorMap tm_qbuf;
   WeightMap tm_lm_w;
   // staged step
   int S = 0, B = 0, n_logit = 0, bt_stride = 0, n_items = 0, n_comb = 0, n_tile_items = 0, n_row_items = 0;
@@ -266,10 +274,10 @@ int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char*
 
 // GEMM against a weight: (N tile, K splits) from the autotuned table for this M bucket (or the
 // analytic planner before autotune), then launch with the matching tensor map.
-cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
+cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
                    cudaStream_t s, float* splitk_ws, int64_t splitk_cap, const GemmTable* tune = nullptr,
                    int kind = -1) {
-  ag::GemmPlan p{0, 0};
+  ag::GemmPlan p{0, 0, 128};
   if (tune && tune->ready && kind >= 0) {
     for (size_t i = 0; i < tune->m_bucket.size(); ++i) {
       if (M <= tune->m_bucket[i] || i + 1 == tune->m_bucket.size()) {
@@ -278,10 +286,17 @@ cudaError_t gemm_w(const CUtensorMap& a, const WeightMap& w, int M, int N, int K
       }
     }
     if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
+    if (M > p.am) p.am = 128;
   }
   if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
   if (p.bn == 256 && !w.has256) p.bn = 128;
-  return ag::launch_gemm(a, w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws);
+  return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
+}
+
+int32_t amap(ActMap* a, const void* ptr, int64_t rows, int64_t k, const char* what) {
+  AG_TRY(tmap(&a->box32, ptr, rows, k, 32, what));
+  AG_TRY(tmap(&a->box64, ptr, rows, k, 64, what));
+  return tmap(&a->box128, ptr, rows, k, 128, what);
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -329,6 +344,24 @@ void prof_harvest(ag_model* m) {
     }
   }
   m->prof_pending.clear();
+}
+
+// AG_DEBUG_SYNC=1: synchronise after every launch of the forward and name the failing kernel.
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("AG_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+int32_t dbg(cudaStream_t s, const char* what, int layer) {
+  if (!debug_sync()) return AG_OK;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess)
+    return fail(AG_ECUDA, std::string("AG_DEBUG_SYNC: ") + what + " (layer " + std::to_string(layer) + "): " +
+                              cudaGetErrorString(e));
+  return AG_OK;
 }
 
 double gemm_flops(int M, int N, int K) { return 2.0 * M * static_cast<double>(N) * K; }
@@ -401,10 +434,10 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   chk(dmalloc(&m->meta_dev, m->meta_cap));
   if (r == AG_OK && cudaMallocHost(&m->tok_host, Sq * sizeof(int32_t)) != cudaSuccess) r = fail(AG_EALLOC, "pinned");
   if (r == AG_OK) {
-    chk(tmap(&m->tm_xln, m->xln, T, c.hidden, 128, "xln"));
-    chk(tmap(&m->tm_attn, m->attn, T, m->hq, 128, "attn"));
-    chk(tmap(&m->tm_ffn, m->ffn, T, m->ffn_l, 128, "ffn"));
-    chk(tmap(&m->tm_lm_in, m->lm_in, Sq, c.hidden, 128, "lm_in"));
+    chk(amap(&m->tm_xln, m->xln, T, c.hidden, "xln"));
+    chk(amap(&m->tm_attn, m->attn, T, m->hq, "attn"));
+    chk(amap(&m->tm_ffn, m->ffn, T, m->ffn_l, "ffn"));
+    chk(amap(&m->tm_lm_in, m->lm_in, Sq, c.hidden, "lm_in"));
     chk(tmap(&m->tm_qbuf, m->qbuf, T, m->hq, 128, "q buffer"));
   }
   if (r == AG_OK) {
@@ -635,6 +668,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ep.block_size = c.block_size;
         ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
         AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmQkv));
+        AG_TRY(dbg(s, "qkv_gemm", l));
       }
       {
         ag::AttnParams ap;
@@ -659,6 +693,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ProfScope ps(m, AG_K_ATTENTION, s, m->attn_flops_step, m->attn_bytes_step);
         if (m->n_comb > 0) m->launches_last += 1;
         AG_CUDA(ag::launch_attention(ap, atm, m->d_items, m->n_tile_items, m->n_row_items, m->d_comb, m->n_comb, s));
+        AG_TRY(dbg(s, "attention", l));
       }
       {
         // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
@@ -674,6 +709,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         }
         ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
         AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmOut));
+        AG_TRY(dbg(s, "out_gemm", l));
       }
       if (tp) {
         {
@@ -697,6 +733,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e1.ldc = m->ffn_l;
         ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
         AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc1));
+        AG_TRY(dbg(s, "fc1_gemm", l));
       }
       {
         ag::GemmEpilogue e2;
@@ -711,6 +748,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         }
         ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
         AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc2));
+        AG_TRY(dbg(s, "fc2_gemm", l));
       }
       if (tp) {
         ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
@@ -740,6 +778,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     {
       ProfScope ps(m, AG_K_LMHEAD_GEMM, s, gemm_flops(NL, m->vocab_l, H), gemm_bytes(NL, m->vocab_l, H, 4));
       AG_CUDA(gemm_w(m->tm_lm_in, m->tm_lm_w, NL, m->vocab_l, H, el, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmLm));
+      AG_TRY(dbg(s, "lm_head", -1));
     }
     if (!tp) {
       ProfScope ps(m, AG_K_ARGMAX, s, 0.0, 4.0 * NL * m->vocab_l);
@@ -807,7 +846,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   AG_CUDA(cudaMemsetAsync(m->lm_in, 0, align_up(c.max_seqs, 128) * H * 2, s));
   const LayerState& L0 = m->layers[0];
   struct Shape {
-    const CUtensorMap* a;
+    const ActMap* a;
     const WeightMap* w;
     int N, K, mcap;
     void* out;
@@ -819,13 +858,19 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       {&m->tm_ffn, &L0.tm_fc2, H, m->ffn_l, c.max_tokens, m->proj, 0},
       {&m->tm_lm_in, &m->tm_lm_w, m->vocab_l, H, c.max_seqs, m->logits, 1},
   };
-  const ag::GemmPlan cands[] = {{256, 1}, {128, 1}, {64, 1}, {256, 2}, {128, 2}, {64, 2}, {256, 3},
-                                {256, 4}, {128, 4}, {64, 4}, {256, 6}, {128, 6}, {256, 8}, {128, 8}};
+  std::vector<ag::GemmPlan> cands;
+  for (int am : {128, 64, 32})
+    for (const ag::GemmPlan& q : {ag::GemmPlan{256, 1}, ag::GemmPlan{128, 1}, ag::GemmPlan{64, 1},
+                                  ag::GemmPlan{256, 2}, ag::GemmPlan{128, 2}, ag::GemmPlan{64, 2},
+                                  ag::GemmPlan{256, 3}, ag::GemmPlan{256, 4}, ag::GemmPlan{128, 4},
+                                  ag::GemmPlan{64, 4}, ag::GemmPlan{256, 6}, ag::GemmPlan{128, 6},
+                                  ag::GemmPlan{256, 8}, ag::GemmPlan{128, 8}})
+      cands.push_back({q.bn, q.k_splits, am});
   cudaEvent_t e0, e1;
   AG_CUDA(cudaEventCreate(&e0));
   AG_CUDA(cudaEventCreate(&e1));
   for (int k = 0; k < kGemmKinds; ++k) {
-    t.plan[k].assign(t.m_bucket.size(), ag::GemmPlan{256, 1});
+    t.plan[k].assign(t.m_bucket.size(), ag::GemmPlan{256, 1, 128});
     const Shape& sh = shapes[k];
     for (size_t b = 0; b < t.m_bucket.size(); ++b) {
       const int M = std::min(t.m_bucket[b], sh.mcap);
@@ -836,16 +881,18 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       float best = 1e30f;
       for (const ag::GemmPlan& p : cands) {
         if (p.bn == 256 && !sh.w->has256) continue;
+        if (M > p.am) continue;
         const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
         if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
         if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
         const CUtensorMap& wm = sh.w->box(p.bn);
+        const CUtensorMap& am = sh.a->box(p.am);
         for (int rep = 0; rep < 2; ++rep)
-          AG_CUDA(ag::launch_gemm(*sh.a, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws));
+          AG_CUDA(ag::launch_gemm(am, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws, p.am));
         const int iters = 5;
         AG_CUDA(cudaEventRecord(e0, s));
         for (int rep = 0; rep < iters; ++rep)
-          AG_CUDA(ag::launch_gemm(*sh.a, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws));
+          AG_CUDA(ag::launch_gemm(am, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws, p.am));
         AG_CUDA(cudaEventRecord(e1, s));
         AG_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;
@@ -873,7 +920,7 @@ int32_t ag_model_get_gemm_plans(ag_model* m, int32_t* out, int32_t cap) {
         out[4 * n] = k;
         out[4 * n + 1] = m->tune.m_bucket[b];
         out[4 * n + 2] = m->tune.plan[k][b].bn;
-        out[4 * n + 3] = m->tune.plan[k][b].k_splits;
+        out[4 * n + 3] = m->tune.plan[k][b].k_splits + 100 * m->tune.plan[k][b].am;
       }
       ++n;
     }
@@ -903,7 +950,11 @@ int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, fl
 // ---------------------------------------------------------------- standalone kernels
 int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias, const void* residual,
                      int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32, int32_t M, int32_t N, int32_t K,
-                     int32_t block_n, int32_t k_splits, void* workspace, int64_t workspace_bytes, void* stream) {
+                     int32_t block_n, int32_t k_splits, int32_t a_rows, void* workspace, int64_t workspace_bytes,
+                     void* stream) {
+  if (a_rows == 0) a_rows = 128;
+  if (a_rows != 32 && a_rows != 64 && a_rows != 128) return fail(AG_EINVAL, "a_rows must be 32, 64 or 128");
+  if (M > a_rows) return fail(AG_EINVAL, "a_rows < M");
   if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");
   if (M < 0 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0) return fail(AG_EINVAL, "need N%32==0, K%8==0");
   const int64_t cap = workspace ? workspace_bytes / 4 : 0;
@@ -922,7 +973,7 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
   }
   if (block_n != 64 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 64, 128 or 256");
   CUtensorMap ta, tb;
-  int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, 128);
+  int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, a_rows);
   if (r) return fail(AG_EINVAL, "tensor map A failed (alignment?)");
   r = ag::make_tmap_kmajor(&tb, W, N, K, ldw, block_n);
   if (r) return fail(AG_EINVAL, "tensor map W failed (alignment?)");
@@ -935,7 +986,7 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
   ep.ldc = ldd;
   ep.out_f32 = out_f32;
   AG_CUDA(ag::launch_gemm(ta, tb, M, N, K, block_n, ep, 0, static_cast<cudaStream_t>(stream), k_splits,
-                          static_cast<float*>(workspace)));
+                          static_cast<float*>(workspace), a_rows));
   return AG_OK;
 }
 

@@ -22,12 +22,16 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kThreads = 256;
 
-template <int BN>
+// AM = activation rows TMA-loaded per stage.  AM < 128 is the small-M (weight streaming)
+// variant: the M=128 UMMA still reads a 128-row A window, whose rows >= AM are stale smem that
+// only feeds masked output rows, so ~4x more weight bytes fit in the ring.
+template <int BN, int AM = 128>
 struct GemmCfg {
-  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kABytes = AM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesFit = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256;
 };
@@ -117,12 +121,12 @@ AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const u
   }
 }
 
-template <int BN>
+template <int BN, int AM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K,
                         GemmEpilogue ep, int k_splits, float* __restrict__ partial) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, AM>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -238,8 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * kBM + ew * 32 + lane;
+      const bool warp_live = m_blk * kBM + ew * 32 < M;  // whole warp beyond M: nothing to drain
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < (warp_live ? BN / 32 : 0); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
@@ -344,14 +349,14 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int BN>
+template <int BN, int AM = 128>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                              const GemmEpilogue& ep, int k_splits, float* partial, int max_ctas,
                              cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, AM>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, AM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -360,7 +365,7 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (units < grid) grid = units;
-  gemm_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
+  gemm_bf16_tn_kernel<BN, AM><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 32);
@@ -370,9 +375,21 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
 }
 
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
-                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial) {
+                        const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial,
+                        int am) {
   if (M <= 0) return cudaSuccess;
   if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
+  if (am != 128 && M > am) return cudaErrorInvalidValue;  // small-M variant needs one m-block
+  if (am == 32) {
+    if (bn == 256) return launch_bn<256, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    if (bn == 64) return launch_bn<64, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    return launch_bn<128, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+  }
+  if (am == 64) {
+    if (bn == 256) return launch_bn<256, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    if (bn == 64) return launch_bn<64, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    return launch_bn<128, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+  }
   if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   if (bn == 64) return launch_bn<64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);

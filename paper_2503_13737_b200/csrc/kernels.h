@@ -36,12 +36,15 @@ int num_sms();
 int pick_block_n(int M, int N);
 // k_splits > 1 writes fp32 partials to `partial` (k_splits * M * N floats) and a reduce kernel
 // applies the epilogue; choose (bn, k_splits) with plan_gemm.
+// am = activation rows loaded per stage (128; or 32/64 for the small-M variant, which needs M <= am
+// and an A tensor map whose box has `am` rows).
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits = 1,
-                        float* partial = nullptr);
+                        float* partial = nullptr, int am = 128);
 struct GemmPlan {
   int bn;
   int k_splits;
+  int am = 128;
 };
 GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats);
 

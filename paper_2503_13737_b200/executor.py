@@ -99,7 +99,9 @@ class CudaExecutor:
         kinds = ("qkv", "out", "fc1", "fc2", "lm_head")
         buf = (C.c_int32 * (4 * 512))()
         n = int(self.lib.ag_model_get_gemm_plans(self.handle, buf, 512))
-        return [(kinds[buf[4 * i]], buf[4 * i + 1], buf[4 * i + 2], buf[4 * i + 3]) for i in range(min(n, 512))]
+        # (kind, m_bucket, block_n, k_splits, a_rows)
+        return [(kinds[buf[4 * i]], buf[4 * i + 1], buf[4 * i + 2], buf[4 * i + 3] % 100, buf[4 * i + 3] // 100)
+                for i in range(min(n, 512))]
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -39,7 +39,7 @@ def _workspace(device, nbytes: int) -> torch.Tensor:
 
 def gemm(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, residual: torch.Tensor | None = None,
          relu: bool = False, out_f32: bool = False, out: torch.Tensor | None = None, block_n: int = 0,
-         k_splits: int = 0) -> torch.Tensor:
+         k_splits: int = 0, a_rows: int = 0) -> torch.Tensor:
     """D = a @ w.T (+bias) (+residual) (relu) on the tcgen05 GEMM; a [M,K], w [N,K] bf16.
     block_n / k_splits 0 = planned by the library (split-K partials in a cached workspace)."""
     _need_cuda(a, w, bias, residual, out)
@@ -55,7 +55,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, res
     _lib.check(_lib.load().ag_gemm_bf16(
         a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), _ptr(bias), _ptr(residual),
         residual.stride(0) if residual is not None else 0, int(relu), out.data_ptr(), out.stride(0), int(out_f32),
-        M, N, K, block_n, k_splits, ws.data_ptr(), ws.numel(), _stream()))
+        M, N, K, block_n, k_splits, a_rows, ws.data_ptr(), ws.numel(), _stream()))
     return out
 
 

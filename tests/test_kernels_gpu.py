@@ -42,6 +42,20 @@ def test_gemm_matches_fp32(K, M, N, K_, bn, splits):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
 
 
+@pytest.mark.parametrize("M,N,K_,bn,splits,a_rows", [(1, 5120, 5120, 128, 1, 32), (32, 15360, 5120, 256, 2, 32),
+                                                     (60, 2048, 20480, 64, 4, 64), (64, 20480, 5120, 256, 1, 64)])
+def test_gemm_small_m_variant(K, M, N, K_, bn, splits, a_rows):
+    """Small-M path: only `a_rows` activation rows are staged; stale rows feed masked outputs only."""
+    a, w = _bf((M, K_), 21), _bf((N, K_), 22, 0.05)
+    bias, res = _bf((N,), 23), _bf((M, N), 24)
+    ref = a.float() @ w.float().T + bias.float() + res.float()
+    out = K.gemm(a.to(DEV), w.to(DEV), bias=bias.to(DEV), residual=res.to(DEV), block_n=bn, k_splits=splits,
+                 a_rows=a_rows)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    assert (out.float().cpu() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
 @pytest.mark.parametrize("bn,splits", [(256, 1), (128, 4), (64, 2)])
 def test_gemm_epilogue_bias_residual_relu_f32(K, bn, splits):
     M, N, K_ = 300, 1024, 768

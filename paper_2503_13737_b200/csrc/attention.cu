@@ -336,10 +336,13 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
         s[c] = c < lim ? s[c] * kLog2e : -INFINITY;
         mx = fmaxf(mx, s[c]);
       }
-      if (mx > m_used + kRescaleThresh) {
-        // the running max grew: rescale l and the O row (after every earlier P.V finished)
-        const float alpha = exp2f(m_used - mx);  // 0 on the first visit (m_used = -inf)
-        if (j > 0 && m_used != -INFINITY) {
+      // Lazy rescale: a row whose running max grew by more than 2^8 rescales l and its O row
+      // (after every earlier P.V finished).  tcgen05.ld/st are .sync.aligned, so the decision to
+      // touch TMEM is warp-uniform; rows that did not grow scale by 1.
+      const bool grow = mx > m_used + kRescaleThresh;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? exp2f(m_used - mx) : 1.0f;  // 0 on a row's first visit
+        if (__any_sync(0xffffffffu, grow && j > 0 && m_used != -INFINITY)) {
           mbar_wait(&bars->o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
@@ -354,8 +357,10 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
           tmem_st_wait();
           tc_fence_before();
         }
-        l *= alpha;
-        m_used = mx;
+        if (grow) {
+          l *= alpha;
+          m_used = mx;
+        }
       }
       const float mref = m_used == -INFINITY ? 0.f : m_used;
       // P_j -> smem buffer (j & 1), free once P.V of tile j-2 completed

@@ -954,7 +954,7 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
                      void* stream) {
   if (a_rows == 0) a_rows = 128;
   if (a_rows != 32 && a_rows != 64 && a_rows != 128) return fail(AG_EINVAL, "a_rows must be 32, 64 or 128");
-  if (M > a_rows) return fail(AG_EINVAL, "a_rows < M");
+  if (a_rows != 128 && M > a_rows) return fail(AG_EINVAL, "a_rows < M");
   if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");
   if (M < 0 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0) return fail(AG_EINVAL, "need N%32==0, K%8==0");
   const int64_t cap = workspace ? workspace_bytes / 4 : 0;

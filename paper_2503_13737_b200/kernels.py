@@ -71,17 +71,18 @@ def kv_append(k: torch.Tensor, v: torch.Tensor, slot_mapping: torch.Tensor, k_po
 
 def paged_attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor,
                     cu_q: torch.Tensor, ctx_len: torch.Tensor, out: torch.Tensor | None = None,
-                    workspace_bytes: int = 64 << 20) -> torch.Tensor:
+                    workspace_bytes: int = 64 << 20, workspace: torch.Tensor | None = None,
+                    device_meta: tuple[torch.Tensor, torch.Tensor] | None = None) -> torch.Tensor:
     """Mixed prefill/decode paged attention; q [S, heads*128] already scaled; cu_q/ctx_len int32 (CPU)."""
     _need_cuda(q, k_pool, v_pool, block_table)
     heads = k_pool.shape[1]
     cu_q_h = cu_q.to(torch.int32).cpu().contiguous()
     ctx_h = ctx_len.to(torch.int32).cpu().contiguous()
-    cu_q_d = cu_q_h.to(q.device)
-    ctx_d = ctx_h.to(q.device)
+    cu_q_d, ctx_d = device_meta if device_meta is not None else (cu_q_h.to(q.device), ctx_h.to(q.device))
     if out is None:
         out = torch.zeros(q.shape[0], heads * 128, device=q.device, dtype=torch.bfloat16)
-    ws = torch.empty(workspace_bytes, device=q.device, dtype=torch.uint8)
+    ws = workspace if workspace is not None else torch.empty(workspace_bytes, device=q.device, dtype=torch.uint8)
+    workspace_bytes = ws.numel()
     _lib.check(_lib.load().ag_paged_attention(
         q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(), k_pool.shape[0], block_table.data_ptr(),
         block_table.stride(0),

@@ -286,10 +286,11 @@ cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, con
       }
     }
     if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
-    if (M > p.am) p.am = 128;
+    if (p.am < 128 && M > p.am) p.am = 128;
   }
   if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
-  if (p.bn == 256 && !w.has256) p.bn = 128;
+  if (p.bn == 256 && !w.has256 && p.am != 256) p.bn = 128;
+  if (p.am == 256) return ag::launch_gemm(a.box(128), w.box(p.bn / 2), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, 256);
   return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
 }
 
@@ -859,7 +860,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       {&m->tm_lm_in, &m->tm_lm_w, m->vocab_l, H, c.max_seqs, m->logits, 1},
   };
   std::vector<ag::GemmPlan> cands;
-  for (int am : {128, 64, 32})
+  for (int am : {256, 128, 64, 32})
     for (const ag::GemmPlan& q : {ag::GemmPlan{256, 1}, ag::GemmPlan{128, 1}, ag::GemmPlan{64, 1},
                                   ag::GemmPlan{256, 2}, ag::GemmPlan{128, 2}, ag::GemmPlan{64, 2},
                                   ag::GemmPlan{256, 3}, ag::GemmPlan{256, 4}, ag::GemmPlan{128, 4},
@@ -880,13 +881,14 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       ep.out_f32 = sh.out_f32;
       float best = 1e30f;
       for (const ag::GemmPlan& p : cands) {
-        if (p.bn == 256 && !sh.w->has256) continue;
-        if (M > p.am) continue;
+        if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
+        if (p.bn == 256 && !sh.w->has256 && p.am != 256) continue;
+        if (p.am < 128 && M > p.am) continue;
         const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
         if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
         if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
-        const CUtensorMap& wm = sh.w->box(p.bn);
-        const CUtensorMap& am = sh.a->box(p.am);
+        const CUtensorMap& wm = sh.w->box(p.am == 256 ? p.bn / 2 : p.bn);
+        const CUtensorMap& am = sh.a->box(p.am == 256 ? 128 : p.am);
         for (int rep = 0; rep < 2; ++rep)
           AG_CUDA(ag::launch_gemm(am, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws, p.am));
         const int iters = 5;
@@ -953,8 +955,10 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
                      int32_t block_n, int32_t k_splits, int32_t a_rows, void* workspace, int64_t workspace_bytes,
                      void* stream) {
   if (a_rows == 0) a_rows = 128;
-  if (a_rows != 32 && a_rows != 64 && a_rows != 128) return fail(AG_EINVAL, "a_rows must be 32, 64 or 128");
-  if (a_rows != 128 && M > a_rows) return fail(AG_EINVAL, "a_rows < M");
+  if (a_rows != 32 && a_rows != 64 && a_rows != 128 && a_rows != 256)
+    return fail(AG_EINVAL, "a_rows must be 32, 64, 128 or 256 (CTA pair)");
+  if (a_rows < 128 && M > a_rows) return fail(AG_EINVAL, "a_rows < M");
+  if (a_rows == 256 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "CTA pair needs block_n 128/256");
   if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");
   if (M < 0 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0) return fail(AG_EINVAL, "need N%32==0, K%8==0");
   const int64_t cap = workspace ? workspace_bytes / 4 : 0;
@@ -973,9 +977,9 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
   }
   if (block_n != 64 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 64, 128 or 256");
   CUtensorMap ta, tb;
-  int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, a_rows);
+  int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, a_rows == 256 ? 128 : a_rows);
   if (r) return fail(AG_EINVAL, "tensor map A failed (alignment?)");
-  r = ag::make_tmap_kmajor(&tb, W, N, K, ldw, block_n);
+  r = ag::make_tmap_kmajor(&tb, W, N, K, ldw, a_rows == 256 ? block_n / 2 : block_n);
   if (r) return fail(AG_EINVAL, "tensor map W failed (alignment?)");
   ag::GemmEpilogue ep;
   ep.bias = static_cast<const bf16*>(bias);

@@ -275,6 +275,178 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// A cluster of two CTAs on one TPC computes a 256 x BN tile with tcgen05.mma.cta_group::2 (M=256):
+// each CTA stages its own 128 activation rows and BN/2 weight rows per k-block, so a CTA moves
+// (128 + BN/2) x 64 x 2 bytes through TMA per 128 x BN outputs instead of (128 + BN) x 64 x 2 --
+// a third less L2->SMEM traffic at BN=256, which is what bounds the 1-CTA kernel at large M.
+// The leader (rank 0) issues the MMAs; its commits multicast to both CTAs' barriers.  Each CTA's
+// epilogue drains its own TMEM (rows 128*rank ..) exactly like the 1-CTA kernel.
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int kABytes = 128 * kBK * 2;
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesFit = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 10 ? 10 : kStagesFit;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 256;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                         int M, int N, int K, GemmEpilogue ep, int k_splits, float* __restrict__ partial) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int num_pairs = gridDim.x >> 1;
+  const int num_m = (M + 255) / 256;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_kb_total = (K + kBK - 1) / kBK;
+  const int kb_per = (num_kb_total + k_splits - 1) / k_splits;
+  const int num_tiles = num_m * num_n * k_splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_cg2(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs): own 128 A rows + own BN/2 B rows per k-block
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_w = num_m <= 1 ? policy_evict_first() : policy_evict_normal();
+      const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < num_tiles; t += num_pairs) {
+        const int m_blk = t % num_m;
+        const int ks = (t / num_m) % k_splits;
+        const int n_blk = t / (num_m * k_splits);
+        const int kb0 = ks * kb_per;
+        const int kb1 = min(num_kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          const uint32_t fb = full0 + stage * 8;
+          tma_load_2d_cg2(sA + stage * Cfg::kABytes, &tmap_a, fb, kb * kBK, m_blk * 256 + rank * 128, pol_a);
+          tma_load_2d_cg2(sB + stage * Cfg::kBBytes, &tmap_b, fb, kb * kBK, n_blk * BN + rank * (BN / 2), pol_w);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: leader CTA only, one thread
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < num_tiles; t += num_pairs) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int ks = (t / num_m) % k_splits;
+        const int kb0 = ks * kb_per;
+        const int kb1 = min(num_kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * Cfg::kABytes));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * Cfg::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_ss_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit_cg2(&empty_bar[stage], 0x3);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_cg2(&tfull_bar[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256-row tile
+    const int ew = warp - 4;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < num_tiles; t += num_pairs) {
+      const int m_blk = t % num_m;
+      const int ks = (t / num_m) % k_splits;
+      const int n_blk = t / (num_m * k_splits);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = m_blk * 256 + static_cast<int>(rank) * 128 + ew * 32;
+      const int row = row0 + lane;
+      const bool warp_live = row0 < M;
+#pragma unroll 1
+      for (int c = 0; c < (warp_live ? BN / 32 : 0); ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int col0 = n_blk * BN + c * 32;
+        if (row < M && col0 < N) {
+          if (k_splits == 1) {
+            epilogue_chunk(ep, row, col0, r);
+          } else {
+            float* dst = partial + ((size_t)ks * M + row) * N + col0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) st_global_v4(dst + q * 4, r[q * 4], r[q * 4 + 1], r[q * 4 + 2], r[q * 4 + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, Cfg::kTmemCols);
+  }
+}
+
 // Sum the K-split fp32 partials of 32 consecutive columns and apply the fused epilogue.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M,
                                                             int N, GemmEpilogue ep) {
@@ -374,10 +546,41 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   return cudaGetLastError();
 }
 
+template <int BN>
+static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                              const GemmEpilogue& ep, int k_splits, float* partial, int max_ctas,
+                              cudaStream_t stream) {
+  using Cfg = Gemm2Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm2_bf16_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * k_splits;
+  int grid = num_sms() & ~1;
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas & ~1;
+  if (2 * units < grid) grid = 2 * units;
+  gemm2_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || k_splits == 1) return e;
+  const int64_t work = static_cast<int64_t>(M) * (N / 32);
+  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+  splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial,
                         int am) {
   if (M <= 0) return cudaSuccess;
+  if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
+    if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
+    if (bn == 256) return launch_bn2<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    if (bn == 128) return launch_bn2<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    return cudaErrorInvalidValue;
+  }
   if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
   if (am != 128 && M > am) return cudaErrorInvalidValue;  // small-M variant needs one m-block
   if (am == 32) {

@@ -37,7 +37,8 @@ int pick_block_n(int M, int N);
 // k_splits > 1 writes fp32 partials to `partial` (k_splits * M * N floats) and a reduce kernel
 // applies the epilogue; choose (bn, k_splits) with plan_gemm.
 // am = activation rows loaded per stage (128; or 32/64 for the small-M variant, which needs M <= am
-// and an A tensor map whose box has `am` rows).
+// and an A tensor map whose box has `am` rows).  am = 256 selects the CTA-pair kernel (256 x bn
+// tiles, bn in {128, 256}): then ta's box has 128 rows and tb's box bn/2 rows.
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits = 1,
                         float* partial = nullptr, int am = 128);

@@ -65,15 +65,16 @@ def sweep(cfg, tp: int = 1, sizes=SWEEP, seq_len: int = 512, reps: int = 5, exec
 
 
 def fit(points: list[dict], hidden: int, num_layers: int, kvc_tokens: int, gain: float = 0.03) -> dict:
-    """Least-squares T = T_0 + a*S_f over the sweep; S_pf = smallest size whose throughput is within
+    """Least-squares T = T_0 + a*S_f over the sweep, weighted by 1/T (relative error, so the model
+    is as accurate for a 64-token decode step as for a pivot-sized one: TTFT SLOs of short prompts
+    come from the small end, workload.py base_ttft); S_pf = smallest size whose throughput is within
     `gain` of the best measured (the paper's <3% marginal-gain saturation rule)."""
     s = np.array([p["s_f"] for p in points], float)
     t = np.array([p["seconds"] for p in points], float)
     thr = s / t
     best = thr.max()
     s_pf = int(s[np.argmax(thr >= (1.0 - gain) * best)])
-    big = s >= 256
-    a, t0 = np.polyfit(s[big], t[big], 1)
+    a, t0 = np.polyfit(s, t, 1, w=1.0 / t)
     t0 = max(0.0, float(t0))
     return {"hidden_size": hidden, "num_layers": num_layers, "pivot_forward_size": s_pf,
             "pivot_time_s": float(a * s_pf), "bytes_per_element": 2, "fixed_overhead_s": t0,

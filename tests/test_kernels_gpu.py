@@ -56,6 +56,19 @@ def test_gemm_small_m_variant(K, M, N, K_, bn, splits, a_rows):
     assert (out.float().cpu() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
 
 
+@pytest.mark.parametrize("M,N,K_,bn,splits", [(256, 512, 256, 256, 1), (300, 1920, 640, 128, 1), (1000, 5120, 1024, 256, 1),
+                                              (777, 2560, 5120, 256, 2), (2048, 3072, 5120, 128, 1), (129, 768, 512, 256, 1)])
+def test_gemm_cta_pair(K, M, N, K_, bn, splits):
+    """CTA-pair (cta_group::2, 256-row tiles) kernel with bias + residual epilogue vs fp32."""
+    a, w = _bf((M, K_), 31), _bf((N, K_), 32, 0.05)
+    bias, res = _bf((N,), 33), _bf((M, N), 34)
+    ref = a.float() @ w.float().T + bias.float() + res.float()
+    out = K.gemm(a.to(DEV), w.to(DEV), bias=bias.to(DEV), residual=res.to(DEV), block_n=bn, k_splits=splits,
+                 a_rows=256)
+    torch.cuda.synchronize()
+    assert (out.float().cpu() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
 @pytest.mark.parametrize("bn,splits", [(256, 1), (128, 4), (64, 2)])
 def test_gemm_epilogue_bias_residual_relu_f32(K, bn, splits):
     M, N, K_ = 300, 1024, 768

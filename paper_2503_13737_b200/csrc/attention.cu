@@ -14,8 +14,8 @@
 //    Warp roles (192 threads): w0 TMA producer | w1 MMA issuer + TMEM owner | w2..w5 softmax.
 //
 //  * ROW CTAs (six (row, head, KV split) units per CTA, one per warp): decode tokens and rows
-//    of tiny chunks.  Each warp streams its KV range through its own cp.async ring of 16-token
-//    half pages and computes the dot products and PV on CUDA cores -- this path is HBM-bound.
+//    of tiny chunks.  Each warp streams its KV range page by page through its own 2-deep TMA ring
+//    and runs QK^T / PV on mma.sync with the query as row 0 of the A tile -- this path is HBM-bound.
 //
 // Split-KV partial rows (O normalised, plus (m, l) in the log2 domain) are merged by
 // attn_combine_kernel.  Causality: query row i of a chunk sits at position ctx_len + q_start + i.
@@ -41,12 +41,15 @@ constexpr int kStageBytes = 4 * kSub;
 constexpr int kPOff = kKVOff + 2 * kStageBytes;     // P: 2 buffers x 2 sub-tiles (tokens 0-63, 64-127)
 constexpr int kBarOff = kPOff + 4 * kSub;           // 224 KB
 constexpr int kTileSmem = kBarOff + 256;
-// ---- row path layout
-constexpr int kDecHalf = 16;
-constexpr int kDecSlotBytes = 2 * kDecHalf * kRowBytes;  // K + V = 8 KB
-constexpr int kDecStages = 4;
-constexpr int kDecWarpBytes = kDecStages * kDecSlotBytes;  // 32 KB per warp, 6 warps = 192 KB
-constexpr int kSmemBytes = 1024 + (kTileSmem > 6 * kDecWarpBytes ? kTileSmem : 6 * kDecWarpBytes);
+// ---- row path layout (per warp): kRowStages pages of 32 tokens; a stage is
+//   [K dims 0-63 | K dims 64-127 | V dims 0-63 | V dims 64-127], each 32 rows x 128 B, TMA SW128
+constexpr int kRowStages = 2;
+constexpr int kRowHalf = 32 * 64 * 2;                          // 4 KB
+constexpr int kRowStageBytes = 4 * kRowHalf;                   // 16 KB
+constexpr int kRowWarpBytes = kRowStages * kRowStageBytes;     // 32 KB per warp, 6 warps = 192 KB
+constexpr int kRowBarOff = 6 * kRowWarpBytes;                  // + 6 warps x kRowStages mbarriers
+constexpr int kRowSmem = kRowBarOff + 6 * kRowStages * 8;
+constexpr int kSmemBytes = 1024 + (kTileSmem > kRowSmem ? kTileSmem : kRowSmem);
 
 AG_DEVICE void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -84,117 +87,165 @@ AG_DEVICE uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
 }
 
 // ---------------------------------------------------------------- row (decode) path
-AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnItem& it, int head, uint8_t* wsmem) {
+AG_DEVICE void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+AG_DEVICE void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D += A(16x16, rows 1..15 zero here) . B(16x8), bf16 in, f32 accumulate
+AG_DEVICE void mma_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// Byte offset of 16-B chunk cc (0..7) of row r inside a TMA SWIZZLE_128B [rows][64] bf16 box.
+AG_DEVICE uint32_t sw128(int r, int cc) { return static_cast<uint32_t>(r * 128 + ((cc ^ (r & 7)) << 4)); }
+
+// One warp streams one (query row, head, KV range) unit: TMA brings each 32-token page of K and V
+// (the same SW128 boxes as the tile path) into a 2-deep ring; QK^T and PV run on mma.sync with the
+// single query row as row 0 of the A operand (lanes 0-3 hold it), so a 32-token page costs 32
+// ldmatrix + 64 mma per warp instead of ~1.6k CUDA-core instructions.  Online softmax in the exp2
+// domain; lanes 0-3 own the row's running max, partial sums and O (C-fragment columns 2t, 2t+1).
+AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnTmaps& tm, const AttnItem& it, int head,
+                               uint8_t* wsmem, uint64_t* bars) {
   const int lane = lane_id();
-  const int q0 = p.cu_q[it.seq];
-  const int tok_row = q0 + it.q_start;
+  const int g = lane >> 2, t = lane & 3;
+  const int tok_row = p.cu_q[it.seq] + it.q_start;
   const int qpos = p.ctx_len[it.seq] + it.q_start;
-  const int kv_end = min(it.kv_end, qpos + 1);
-  const int chunk = lane & 15;
-  float qv[8];
-  {
-    const uint4 w = *reinterpret_cast<const uint4*>(p.q + static_cast<int64_t>(tok_row) * p.ldq + head * kHD + chunk * 8);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const float2 f = unpack_bf16x2(ws[h]);
-      qv[2 * h] = f.x * kLog2e;
-      qv[2 * h + 1] = f.y * kLog2e;
-    }
-  }
+  const int kv_lo = it.kv_start;
+  const int kv_hi = min(it.kv_end, qpos + 1);
+  const int pg0 = kv_lo / kPage;
+  const int n_pages = kv_hi > kv_lo ? (kv_hi + kPage - 1) / kPage - pg0 : 0;
   const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
-  const int64_t page_elems = static_cast<int64_t>(p.heads) * kPage * kHD;
-  const int64_t head_off = static_cast<int64_t>(head) * kPage * kHD;
-  const int h0 = it.kv_start / kDecHalf;
-  const int h1 = (kv_end + kDecHalf - 1) / kDecHalf;
   const uint32_t sbase = smem_u32(wsmem);
 
-  auto issue = [&](int h, int slot) {
-    const int page = (h * kDecHalf) / kPage;
-    const int tok0 = (h * kDecHalf) % kPage;
-    const int64_t base = static_cast<int64_t>(bt[page]) * page_elems + head_off + static_cast<int64_t>(tok0) * kHD;
-    const uint32_t sk = sbase + slot * kDecSlotBytes;
-    const uint32_t sv = sk + kDecHalf * kRowBytes;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int id = lane + 32 * i;
-      cp_async16(sk + id * 16, p.kcache + base + id * 8);
-      cp_async16(sv + id * 16, p.vcache + base + id * 8);
-    }
-  };
-
-  float o[4] = {0.f, 0.f, 0.f, 0.f};
-  float m = -INFINITY, l = 0.f;
-  int issued = h0;
-  for (int k = 0; k < kDecStages - 1; ++k) {
-    if (issued < h1) issue(issued, (issued - h0) % kDecStages);
-    ++issued;
-    cp_async_commit();
+  if (lane == 0) {
+    for (int st = 0; st < kRowStages; ++st) mbar_init(&bars[st], 1);
+    fence_barrier_init();
   }
-  for (int h = h0; h < h1; ++h) {
-    if (issued < h1) issue(issued, (issued - h0) % kDecStages);
-    ++issued;
-    cp_async_commit();
-    cp_async_wait<kDecStages - 1>();
-    __syncwarp();
-    const int slot = (h - h0) % kDecStages;
-    const uint8_t* sk = wsmem + slot * kDecSlotBytes;
-    const uint8_t* sv = sk + kDecHalf * kRowBytes;
-    float s_mine = -INFINITY;
+  __syncwarp();
+  auto issue = [&](int i) {  // lane 0: page pg0 + i into stage i % kRowStages
+    const int st = i % kRowStages;
+    const int row = (bt[pg0 + i] * p.heads + head) * kPage;
+    uint8_t* dst = wsmem + st * kRowStageBytes;
+    mbar_arrive_expect_tx(&bars[st], kRowStageBytes);
+    tma_load_2d(dst, &tm.k, &bars[st], 0, row);
+    tma_load_2d(dst + kRowHalf, &tm.k, &bars[st], 64, row);
+    tma_load_2d(dst + 2 * kRowHalf, &tm.v, &bars[st], 0, row);
+    tma_load_2d(dst + 3 * kRowHalf, &tm.v, &bars[st], 64, row);
+  };
+  if (lane == 0)
+    for (int i = 0; i < min(kRowStages, n_pages); ++i) issue(i);
+
+  // q row as the A operand: lanes 0-3 hold dims (16kk + 2t, +1) and (16kk + 8 + 2t, +1)
+  uint32_t qa[8][2];
 #pragma unroll
-    for (int i = 0; i < kDecHalf / 2; ++i) {
-      const int t = 2 * i + (lane >> 4);
-      const uint4 w = *reinterpret_cast<const uint4*>(sk + t * kRowBytes + chunk * 16);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      float d = 0.f;
+  for (int kk = 0; kk < 8; ++kk) qa[kk][0] = qa[kk][1] = 0u;
+  if (g == 0) {
+    const uint32_t* q32 = reinterpret_cast<const uint32_t*>(p.q + static_cast<int64_t>(tok_row) * p.ldq + head * kHD);
 #pragma unroll
-      for (int hh = 0; hh < 4; ++hh) {
-        const float2 f = unpack_bf16x2(ws[hh]);
-        d = fmaf(qv[2 * hh], f.x, d);
-        d = fmaf(qv[2 * hh + 1], f.y, d);
-      }
-#pragma unroll
-      for (int o2 = 8; o2 > 0; o2 >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o2);
-      const float other = __shfl_sync(0xffffffffu, d, (lane & 1) * 16);
-      if ((lane & 15) >> 1 == i) s_mine = other;
+    for (int kk = 0; kk < 8; ++kk) {
+      qa[kk][0] = q32[kk * 8 + t];
+      qa[kk][1] = q32[kk * 8 + 4 + t];
     }
-    const int pos = h * kDecHalf + (lane & 15);
-    if (pos >= kv_end || pos < it.kv_start) s_mine = -INFINITY;
-    float mx = s_mine;
+  }
+  float o[16][4];
 #pragma unroll
-    for (int o2 = 8; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+  for (int d = 0; d < 16; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+  float m = -INFINITY, lpart = 0.f;
+
+  for (int i = 0; i < n_pages; ++i) {
+    const int st = i % kRowStages;
+    mbar_wait(&bars[st], (i / kRowStages) & 1);
+    const uint32_t kb = sbase + st * kRowStageBytes;
+    const uint32_t vb = kb + 2 * kRowHalf;
+    // S = q . K^T for the page's 32 tokens: 4 n-tiles of 8 tokens x 8 k-steps
+    float sc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+      const int r = 8 * j + (lane & 7);
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) {  // 16-B chunks 4mm .. 4mm+3 = k-steps 2mm, 2mm+1
+        const int cg = 4 * mm + (lane >> 3);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + (cg >> 3) * kRowHalf + sw128(r, cg & 7), b0, b1, b2, b3);
+        mma_16816(sc[j], qa[2 * mm][0], qa[2 * mm][1], b0, b1);
+        mma_16816(sc[j], qa[2 * mm + 1][0], qa[2 * mm + 1][1], b2, b3);
+      }
+    }
+    // online softmax over the page (row 0 lives in lanes 0-3: tokens 8j + 2t, +1)
+    const int tok0 = (pg0 + i) * kPage;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = tok0 + 8 * j + 2 * t + e;
+        const bool ok = g == 0 && tok >= kv_lo && tok < kv_hi;
+        sc[j][e] = ok ? sc[j][e] * kLog2e : -INFINITY;
+        mx = fmaxf(mx, sc[j][e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float mnew = fmaxf(m, mx);
     const float mref = mnew == -INFINITY ? 0.f : mnew;
     const float alpha = exp2f(m - mref);
-    const float pe = exp2f(s_mine - mref);
-    float ps = pe;
-#pragma unroll
-    for (int o2 = 8; o2 > 0; o2 >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o2);
-    l = l * alpha + ps;
     m = mnew;
+    uint32_t pa[4];  // P as bf16x2 per n-tile (row 0 only)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] *= alpha;
+    for (int j = 0; j < 4; ++j) {
+      const float p0 = exp2f(sc[j][0] - mref), p1 = exp2f(sc[j][1] - mref);
+      lpart = lpart * (j == 0 ? alpha : 1.f) + p0 + p1;
+      pa[j] = pack_bf16x2(p0, p1);
+    }
 #pragma unroll
-    for (int t = 0; t < kDecHalf; ++t) {
-      const float pt = __shfl_sync(0xffffffffu, pe, t);
-      const uint2 w = *reinterpret_cast<const uint2*>(sv + t * kRowBytes + lane * 8);
-      const float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y);
-      o[0] = fmaf(pt, a.x, o[0]);
-      o[1] = fmaf(pt, a.y, o[1]);
-      o[2] = fmaf(pt, b.x, o[2]);
-      o[3] = fmaf(pt, b.y, o[3]);
+    for (int d = 0; d < 16; ++d) {
+      o[d][0] *= alpha;
+      o[d][1] *= alpha;
+    }
+    // O += P . V: 2 k-steps of 16 tokens x 16 n-tiles of 8 dims (V loaded transposed)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int r = 16 * ks + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int d = 0; d < 16; d += 2) {
+        const int cg = d + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vb + (cg >> 3) * kRowHalf + sw128(r, cg & 7), b0, b1, b2, b3);
+        mma_16816(o[d], pa[2 * ks], pa[2 * ks + 1], b0, b1);
+        mma_16816(o[d + 1], pa[2 * ks], pa[2 * ks + 1], b2, b3);
+      }
     }
     __syncwarp();
+    if (lane == 0 && i + kRowStages < n_pages) {
+      fence_async_smem();
+      issue(i + kRowStages);
+    }
   }
-  cp_async_wait<0>();
+  float l = lpart + __shfl_xor_sync(0xffffffffu, lpart, 1);
+  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  if (g != 0) return;
   const float inv = l > 0.f ? 1.f / l : 0.f;
   if (it.part_row < 0) {
-    __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_row) * p.ldo + head * kHD + lane * 4;
-    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv));
+    __nv_bfloat16* dst = p.out + static_cast<int64_t>(tok_row) * p.ldo + head * kHD + 2 * t;
+#pragma unroll
+    for (int d = 0; d < 16; ++d)
+      *reinterpret_cast<uint32_t*>(dst + 8 * d) = pack_bf16x2(o[d][0] * inv, o[d][1] * inv);
   } else {
     const int64_t prow = static_cast<int64_t>(it.part_row) * p.heads + head;
-    *reinterpret_cast<float4*>(p.part_o + prow * kHD + lane * 4) = make_float4(o[0] * inv, o[1] * inv, o[2] * inv, o[3] * inv);
-    if (lane == 0) {
+    float* dst = p.part_o + prow * kHD + 2 * t;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) *reinterpret_cast<float2*>(dst + 8 * d) = make_float2(o[d][0] * inv, o[d][1] * inv);
+    if (t == 0) {
       p.part_ml[prow * 2] = m;
       p.part_ml[prow * 2 + 1] = l;
     }
@@ -449,31 +500,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int u = (blockIdx.x - n_tile_ctas) * (kThreads / 32) + warp;
   if (u >= n_row_items * p.heads) return;
   const AttnItem itr = items[n_tile_items + u / p.heads];
-  decode_row_warp(p, itr, u % p.heads, smem + warp * kDecWarpBytes);
+  decode_row_warp(p, tm, itr, u % p.heads, smem + warp * kRowWarpBytes,
+                  reinterpret_cast<uint64_t*>(smem + kRowBarOff) + warp * kRowStages);
 }
 
 // Merge split-KV partial rows: out = sum_s w_s O_s / sum_s w_s, w_s = l_s * 2^(m_s - M).
-__global__ void attn_combine_kernel(AttnParams p, const AttnCombine* __restrict__ combines) {
-  const AttnCombine cb = combines[blockIdx.x];
-  const int head = blockIdx.y;
-  const int d = threadIdx.x;
-  for (int r = 0; r < cb.q_rows; ++r) {
-    float mmax = -INFINITY;
-    for (int s = 0; s < cb.n_splits; ++s) {
-      const int64_t prow = static_cast<int64_t>(cb.first_part + s * cb.q_rows + r) * p.heads + head;
-      mmax = fmaxf(mmax, p.part_ml[prow * 2]);
-    }
-    const float mref = mmax == -INFINITY ? 0.0f : mmax;
-    float lsum = 0.0f, acc = 0.0f;
-    for (int s = 0; s < cb.n_splits; ++s) {
-      const int64_t prow = static_cast<int64_t>(cb.first_part + s * cb.q_rows + r) * p.heads + head;
-      const float w = p.part_ml[prow * 2 + 1] * exp2f(p.part_ml[prow * 2] - mref);
-      lsum += w;
-      acc += w * p.part_o[prow * kHD + d];
-    }
-    const float val = lsum > 0.0f ? acc / lsum : 0.0f;
-    p.out[static_cast<int64_t>(cb.tok_row + r) * p.ldo + head * kHD + d] = __float2bfloat16_rn(val);
+// One warp per (query row, head), four head dims per lane; splits of a row sit `q_rows` apart.
+__global__ void __launch_bounds__(256) attn_combine_kernel(AttnParams p, const AttnCombine* __restrict__ combines,
+                                                           int n_combines) {
+  const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (unit >= n_combines * p.heads) return;
+  const int lane = threadIdx.x & 31;
+  const AttnCombine cb = combines[unit / p.heads];
+  const int head = unit % p.heads;
+  float mmax = -INFINITY;
+  for (int sp = 0; sp < cb.n_splits; ++sp) {
+    const int64_t prow = static_cast<int64_t>(cb.first_part + sp * cb.q_rows) * p.heads + head;
+    mmax = fmaxf(mmax, p.part_ml[prow * 2]);
   }
+  const float mref = mmax == -INFINITY ? 0.0f : mmax;
+  float lsum = 0.0f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int sp = 0; sp < cb.n_splits; ++sp) {
+    const int64_t prow = static_cast<int64_t>(cb.first_part + sp * cb.q_rows) * p.heads + head;
+    const float w = p.part_ml[prow * 2 + 1] * exp2f(p.part_ml[prow * 2] - mref);
+    const float4 o = *reinterpret_cast<const float4*>(p.part_o + prow * kHD + lane * 4);
+    lsum += w;
+    acc.x += w * o.x;
+    acc.y += w * o.y;
+    acc.z += w * o.z;
+    acc.w += w * o.w;
+  }
+  const float inv = lsum > 0.0f ? 1.0f / lsum : 0.0f;
+  __nv_bfloat16* dst = p.out + static_cast<int64_t>(cb.tok_row) * p.ldo + head * kHD + lane * 4;
+  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv), pack_bf16x2(acc.z * inv, acc.w * inv));
 }
 
 }  // namespace
@@ -498,7 +558,8 @@ cudaError_t launch_attention(const AttnParams& p, const AttnTmaps& tm, const Att
     if (e != cudaSuccess) return e;
   }
   if (n_combines > 0) {
-    attn_combine_kernel<<<dim3(n_combines, p.heads), kHD, 0, stream>>>(p, combines);
+    const int units = n_combines * p.heads;
+    attn_combine_kernel<<<(units + 7) / 8, 256, 0, stream>>>(p, combines, n_combines);
     return cudaGetLastError();
   }
   return cudaSuccess;

@@ -123,7 +123,7 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
       const int a = s * split;
       out.push_back({t.seq, t.qs, t.rows, a, std::min(t.kv_hi, a + split), base + s * t.rows, 0, 0});
     }
-    w.combines.push_back({cu_q[t.seq] + t.qs, t.rows, base, n_split});
+    for (int r = 0; r < t.rows; ++r) w.combines.push_back({cu_q[t.seq] + t.qs + r, t.rows, base + r, n_split});
     w.part_rows += n_split * t.rows;
   };
   auto split_of = [](int kv_hi, double per_item, int min_len, int align, int& n_split, int& split) {
@@ -845,20 +845,27 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   AG_CUDA(cudaMemsetAsync(m->attn, 0, T * m->hq * 2, s));
   AG_CUDA(cudaMemsetAsync(m->ffn, 0, T * m->ffn_l * 2, s));
   AG_CUDA(cudaMemsetAsync(m->lm_in, 0, align_up(c.max_seqs, 128) * H * 2, s));
-  const LayerState& L0 = m->layers[0];
+  // Candidates are timed on the weights of successive layers (as in the forward), so weight tiles
+  // come from HBM, not from an L2 that still holds the previous repetition's copy.
   struct Shape {
     const ActMap* a;
-    const WeightMap* w;
+    std::vector<const WeightMap*> w;
     int N, K, mcap;
     void* out;
     int out_f32;
   } shapes[kGemmKinds] = {
-      {&m->tm_xln, &L0.tm_qkv, 3 * m->hq, H, c.max_tokens, m->ffn, 0},
-      {&m->tm_attn, &L0.tm_out, H, m->hq, c.max_tokens, m->ffn, 0},
-      {&m->tm_xln, &L0.tm_fc1, m->ffn_l, H, c.max_tokens, m->ffn, 0},
-      {&m->tm_ffn, &L0.tm_fc2, H, m->ffn_l, c.max_tokens, m->proj, 0},
-      {&m->tm_lm_in, &m->tm_lm_w, m->vocab_l, H, c.max_seqs, m->logits, 1},
+      {&m->tm_xln, {}, 3 * m->hq, H, c.max_tokens, m->ffn, 0},
+      {&m->tm_attn, {}, H, m->hq, c.max_tokens, m->ffn, 0},
+      {&m->tm_xln, {}, m->ffn_l, H, c.max_tokens, m->ffn, 0},
+      {&m->tm_ffn, {}, H, m->ffn_l, c.max_tokens, m->proj, 0},
+      {&m->tm_lm_in, {&m->tm_lm_w}, m->vocab_l, H, c.max_seqs, m->logits, 1},
   };
+  for (const LayerState& L : m->layers) {
+    shapes[kGemmQkv].w.push_back(&L.tm_qkv);
+    shapes[kGemmOut].w.push_back(&L.tm_out);
+    shapes[kGemmFc1].w.push_back(&L.tm_fc1);
+    shapes[kGemmFc2].w.push_back(&L.tm_fc2);
+  }
   std::vector<ag::GemmPlan> cands;
   for (int am : {256, 128, 64, 32})
     for (const ag::GemmPlan& q : {ag::GemmPlan{256, 1}, ag::GemmPlan{128, 1}, ag::GemmPlan{64, 1},
@@ -882,19 +889,21 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       float best = 1e30f;
       for (const ag::GemmPlan& p : cands) {
         if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
-        if (p.bn == 256 && !sh.w->has256 && p.am != 256) continue;
+        if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.am < 128 && M > p.am) continue;
         const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
         if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
         if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
-        const CUtensorMap& wm = sh.w->box(p.am == 256 ? p.bn / 2 : p.bn);
+        const int wbox = p.am == 256 ? p.bn / 2 : p.bn;
         const CUtensorMap& am = sh.a->box(p.am == 256 ? 128 : p.am);
-        for (int rep = 0; rep < 2; ++rep)
-          AG_CUDA(ag::launch_gemm(am, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws, p.am));
-        const int iters = 5;
+        const int nw = static_cast<int>(sh.w.size());
+        AG_CUDA(ag::launch_gemm(am, sh.w[nw - 1]->box(wbox), M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws,
+                                p.am));
+        const int iters = 8;
         AG_CUDA(cudaEventRecord(e0, s));
         for (int rep = 0; rep < iters; ++rep)
-          AG_CUDA(ag::launch_gemm(am, wm, M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws, p.am));
+          AG_CUDA(ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits,
+                                  m->splitk_ws, p.am));
         AG_CUDA(cudaEventRecord(e1, s));
         AG_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;

@@ -78,11 +78,11 @@ struct AttnItem {
   int32_t pad0, pad1;
 };
 
-struct AttnCombine {
-  int32_t tok_row;    // global token row of the first row of the tile
-  int32_t q_rows;
+struct AttnCombine {  // one query row whose KV range was split
+  int32_t tok_row;    // global token row
+  int32_t q_rows;     // rows of the split piece: split s of this row is part_row first_part + s * q_rows
   int32_t first_part; // part_row of split 0
-  int32_t n_splits;   // splits are laid out part_row = first_part + s * q_rows
+  int32_t n_splits;
 };
 
 struct AttnParams {

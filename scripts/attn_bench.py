@@ -25,6 +25,10 @@ CASES = {
     "decode_1x100k": [(100000, 1)],
     "mixed": [(4096, 1024)] + [(1500, 1)] * 100 + [(0, 100)] * 10,
     "mixed_small_prompts": [(0, 37), (0, 300), (0, 900), (0, 17), (0, 650)] + [(700, 1)] * 40,
+    "live_dec40": [(2200, 1)] * 40,
+    "live_dec40_fresh300": [(2200, 1)] * 40 + [(0, 300)],
+    "live_dec40_chunk280_on1200": [(2200, 1)] * 40 + [(1200, 280), (0, 20)],
+    "live_dec60_chunk64_on510": [(2100, 1)] * 60 + [(510, 64)],
 }
 
 
@@ -70,6 +74,9 @@ def run(seqs, heads):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 2:  # extra cases recorded from real batches (scripts/make_attn_cases.py)
+        import json as _j
+        CASES.update({k: [tuple(x) for x in v] for k, v in _j.load(open(sys.argv[2])).items()})
     for name, seqs in CASES.items():
         r = run(seqs, HEADS)
         print(json.dumps({"case": name, "heads": HEADS, **r}), flush=True)

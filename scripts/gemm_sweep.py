@@ -13,8 +13,9 @@ for name, (N, Kd) in SHAPES.items():
         out = torch.empty(M, N, device='cuda', dtype=torch.bfloat16)
         ref = (a.float() @ w.float().T)
         row = {"shape": name, "M": M}
-        for bn, ks, am in [(0, 0, 0), (256, 1, 0), (128, 1, 0), (256, 2, 0), (256, 4, 0), (128, 2, 0), (256, 1, 256),
-                           (128, 1, 256), (256, 2, 256)]:
+        for bn, ks, am in [(0, 0, 0), (256, 1, 0), (128, 1, 0), (256, 2, 0), (256, 4, 0), (128, 2, 0), (128, 4, 0),
+                           (64, 4, 0), (128, 8, 0), (256, 1, 256), (128, 1, 256), (256, 2, 256), (128, 2, 256),
+                           (256, 4, 256), (128, 4, 256)]:
             if am == 256 and M < 256:
                 continue
             try:

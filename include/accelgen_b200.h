@@ -138,6 +138,8 @@ AG_API int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, flo
  * the table.  ~1 s at model load.  get_gemm_plans writes (kind, m_bucket, block_n, k_splits) rows. */
 AG_API int32_t ag_model_autotune(ag_model* m, void* stream);
 AG_API int32_t ag_model_get_gemm_plans(ag_model* m, int32_t* out_rows4, int32_t cap);
+/* Install a plan table previously read with get_gemm_plans (same rows; replaces autotune). */
+AG_API int32_t ag_model_set_gemm_plans(ag_model* m, const int32_t* rows4, int32_t n);
 
 /* Per-kernel-class CUDA-event profiling of ag_model_forward (on = 1 resets the counters).
  * get_profile fills up to n entries per class: summed ms, algorithmic FLOPs and HBM bytes, launches. */

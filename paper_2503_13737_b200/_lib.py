@@ -64,6 +64,7 @@ _SIGS = {
     "ag_model_last_launches": (i64, [vp]),
     "ag_model_autotune": (i32, [vp, vp]),
     "ag_model_get_gemm_plans": (i32, [vp, vp, i32]),
+    "ag_model_set_gemm_plans": (i32, [vp, vp, i32]),
     "ag_model_last_h2d_bytes": (i64, [vp]),
     "ag_gemm_bf16": (i32, [vp, i32, vp, i32, vp, vp, i32, i32, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, i64,
                            vp]),

@@ -4,13 +4,13 @@
 //
 //  * TILE CTAs (one per (query tile, head, KV split)): a prefill chunk's rows in tiles of 128.
 //    TMA stages Q (128x128) once and K/V 128 tokens (four 32-token pages) per stage from the
-//    paged pool into a 2-deep SW128 ring.  One thread issues tcgen05.mma:
+//    paged pool into a 3-deep SW128 ring.  One thread issues tcgen05.mma:
 //        S_j  = Q . K_j^T   (M=128, N=128, K=128)  -> TMEM (double-buffered, 2 x 128 columns)
-//        O   += P_j . V_j   (A = P from smem, B = V MN-major)  -> TMEM (128 columns)
+//        O   += P_j . V_j   (A = P from TMEM, B = V MN-major)  -> TMEM (128 columns)
 //    Four softmax warps own one query row per thread: tcgen05.ld the S row, causal/range mask,
 //    online softmax in the exp2 domain with lazy O rescaling (only when the row max grows by
-//    more than 2^8; the rescale is a tcgen05.ld/st round trip of the O row), write P (bf16) into
-//    a double-buffered SW128 smem tile, fence the async proxy, signal the MMA warp.
+//    more than 2^8; the rescale is a tcgen05.ld/st round trip of the O row), tcgen05.st P as
+//    packed bf16 pairs over the first 64 columns of the S buffer, signal the MMA warp.
 //    Warp roles (192 threads): w0 TMA producer | w1 MMA issuer + TMEM owner | w2..w5 softmax.
 //
 //  * ROW CTAs (six (row, head, KV split) units per CTA, one per warp): decode tokens and rows
@@ -38,8 +38,8 @@ constexpr int kSub = 128 * 64 * 2;                  // one [128 rows][64] bf16 S
 constexpr int kQOff = 0;                            // Q: 2 sub-tiles (dims 0-63, 64-127)
 constexpr int kKVOff = 2 * kSub;                    // stage s: K 2 sub-tiles, V 2 sub-tiles (64 KB)
 constexpr int kStageBytes = 4 * kSub;
-constexpr int kPOff = kKVOff + 2 * kStageBytes;     // P: 2 buffers x 2 sub-tiles (tokens 0-63, 64-127)
-constexpr int kBarOff = kPOff + 4 * kSub;           // 224 KB
+constexpr int kKVStages = 3;                        // P lives in TMEM, so three K/V stages fit
+constexpr int kBarOff = kKVOff + kKVStages * kStageBytes;  // 224 KB
 constexpr int kTileSmem = kBarOff + 256;
 // ---- row path layout (per warp): kRowStages pages of 32 tokens; a stage is
 //   [K dims 0-63 | K dims 64-127 | V dims 0-63 | V dims 64-127], each 32 rows x 128 B, TMA SW128
@@ -84,6 +84,15 @@ AG_DEVICE uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;
   return d;
+}
+
+// D(TMEM) (+)= A(TMEM, K-major bf16 pairs per 32-bit column) . B(smem descriptor)
+AG_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 // ---------------------------------------------------------------- row (decode) path
@@ -255,7 +264,7 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnTmaps& tm, const A
 // ---------------------------------------------------------------- tile (tcgen05) path
 struct TileBars {
   uint64_t q_full;
-  uint64_t kv_full[2], kv_empty[2];
+  uint64_t kv_full[kKVStages], kv_empty[kKVStages];
   uint64_t s_full[2], s_empty[2];
   uint64_t p_full[2], o_done[2];
   uint32_t tmem_base;
@@ -275,9 +284,11 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKVStages; ++i) {
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_empty[i], 4);
       mbar_init(&bars->p_full[i], 4);
@@ -302,8 +313,8 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
       const int last_page = (kv_end - 1) / kPage;
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&bars->kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % kKVStages;
+        mbar_wait(&bars->kv_empty[st], ((j / kKVStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->kv_full[st], kStageBytes);
         uint8_t* kdst = smem + kKVOff + st * kStageBytes;
         uint8_t* vdst = kdst + 2 * kSub;
@@ -324,8 +335,8 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       constexpr uint32_t idesc_o = umma_idesc_bf16(kTM, kHD) | (1u << 16);  // B (V) MN-major
       mbar_wait(&bars->q_full, 0);
       auto issue_s = [&](int j) {
-        const int st = j & 1, sbuf = j & 1;
-        mbar_wait(&bars->kv_full[st], (j >> 1) & 1);
+        const int st = j % kKVStages, sbuf = j & 1;
+        mbar_wait(&bars->kv_full[st], (j / kKVStages) & 1);
         mbar_wait(&bars->s_empty[sbuf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t kaddr = sb + kKVOff + st * kStageBytes;
@@ -340,16 +351,16 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       issue_s(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_s(j + 1);
-        const int pb = j & 1, st = j & 1;
+        const int pb = j & 1, st = j % kKVStages;
         mbar_wait(&bars->p_full[pb], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t paddr = sb + kPOff + pb * 2 * kSub;
+        // O += P_j . V_j with P_j (bf16, packed in columns 0-63 of S buffer pb) as the TMEM A operand
+        const uint32_t ptmem = tmem + pb * 128;
         const uint32_t vaddr = sb + kKVOff + st * kStageBytes + 2 * kSub;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA
-          const uint64_t a = umma_desc_sw128(paddr + (k >> 2) * kSub) + 2 * (k & 3);
+        for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA = 8 TMEM columns of packed bf16 pairs
           const uint64_t b = umma_desc_sw128_mn(vaddr + k * 2048, kSub);
-          umma_bf16_ss(tmem + 256, a, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 256, ptmem + 8 * k, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&bars->o_done[pb]);
         umma_commit(&bars->kv_empty[st]);
@@ -414,25 +425,23 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
         }
       }
       const float mref = m_used == -INFINITY ? 0.f : m_used;
-      // P_j -> smem buffer (j & 1), free once P.V of tile j-2 completed
-      if (j >= 2) mbar_wait(&bars->o_done[j & 1], ((j - 2) >> 1) & 1);
-      uint8_t* pbuf = smem + kPOff + (j & 1) * 2 * kSub;
+      // P_j (bf16 pairs) -> columns 0-63 of this tile's S buffer; S_j is already in registers and
+      // the MMA pipe runs P.V_j before the S_{j+2} that next overwrites the buffer (in-order issue)
       float rs = 0.f;
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {  // 16-B chunks of 8 tokens
-        float e[8];
+      for (int half = 0; half < 2; ++half) {
+        uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          e[i] = exp2f(s[ch * 8 + i] - mref);
-          rs += e[i];
+        for (int i = 0; i < 32; ++i) {
+          const float e0 = exp2f(s[half * 64 + 2 * i] - mref), e1 = exp2f(s[half * 64 + 2 * i + 1] - mref);
+          rs += e0 + e1;
+          pk[i] = pack_bf16x2(e0, e1);
         }
-        const int sub = ch >> 3, cc = ch & 7;
-        uint4 v = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]), pack_bf16x2(e[4], e[5]),
-                             pack_bf16x2(e[6], e[7]));
-        *reinterpret_cast<uint4*>(pbuf + sub * kSub + row * 128 + ((cc ^ (row & 7)) << 4)) = v;
+        tmem_st_32x32b_x32(tmem + lane_addr + sbuf * 128 + half * 32, pk);
       }
+      tmem_st_wait();
       l += rs;
-      fence_async_smem();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->p_full[j & 1]);
     }

@@ -938,6 +938,25 @@ int32_t ag_model_get_gemm_plans(ag_model* m, int32_t* out, int32_t cap) {
   return n;
 }
 
+int32_t ag_model_set_gemm_plans(ag_model* m, const int32_t* rows, int32_t n) {
+  if (!m || (n > 0 && !rows)) return fail(AG_EINVAL, "null argument");
+  GemmTable t;
+  for (int i = 0; i < n; ++i) {
+    const int kind = rows[4 * i], mb = rows[4 * i + 1], bn = rows[4 * i + 2], ks = rows[4 * i + 3] % 100,
+              am = rows[4 * i + 3] / 100;
+    if (kind < 0 || kind >= kGemmKinds || mb <= 0 || (bn != 64 && bn != 128 && bn != 256) || ks < 1 ||
+        (am != 32 && am != 64 && am != 128 && am != 256))
+      return fail(AG_EINVAL, "bad gemm plan row " + std::to_string(i));
+    if (kind == 0) t.m_bucket.push_back(mb);
+    t.plan[kind].push_back(ag::GemmPlan{bn, ks, am});
+  }
+  for (int k = 0; k < kGemmKinds; ++k)
+    if (t.plan[k].size() != t.m_bucket.size()) return fail(AG_EINVAL, "plan table is not rectangular");
+  t.ready = !t.m_bucket.empty();
+  m->tune = t;
+  return AG_OK;
+}
+
 int64_t ag_model_last_launches(ag_model* m) { return m ? m->launches_last : -1; }
 int64_t ag_model_last_h2d_bytes(ag_model* m) { return m ? m->h2d_last : -1; }
 

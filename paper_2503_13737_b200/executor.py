@@ -9,7 +9,10 @@ D2H.  There is no CPU fallback: without CUDA or the library this raises EngineFa
 from __future__ import annotations
 
 import ctypes as C
+import json
+import os
 import time
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -73,8 +76,7 @@ class CudaExecutor:
             buf = C.create_string_buffer(bytes(nccl_uid), 128)
             _lib.check(self.lib.ag_model_init_tp(handle, buf))
         if autotune:
-            with torch.cuda.device(self.device):
-                _lib.check(self.lib.ag_model_autotune(handle, torch.cuda.current_stream(self.device).cuda_stream))
+            self._autotune()
         self._dev_ms = C.c_float(0.0)
         self._swapped: dict[int, torch.Tensor] = {}
         self.logits_buf = torch.empty(max_seqs, cfg.vocab // tp_size, dtype=torch.float32, device=self.device) \
@@ -94,6 +96,31 @@ class CudaExecutor:
         _lib.check(self.lib.ag_model_get_profile(self.handle, ms, fl, by, cnt, n))
         return {name: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
                 for i, name in enumerate(_lib.PROF_CLASSES)}
+
+    def _autotune(self) -> None:
+        """Time the GEMM plan candidates on this GPU, or reuse a table cached by an earlier run of the
+        same library on the same GPU model and shapes (AG_GEMM_PLAN_CACHE=<dir>, opt-in)."""
+        cache_dir = os.environ.get("AG_GEMM_PLAN_CACHE")
+        key = None
+        if cache_dir:
+            import hashlib
+            lib_hash = hashlib.sha1(Path(_lib.LIB_PATH).read_bytes()).hexdigest()[:12]
+            cfg = self.cfg
+            key = Path(cache_dir) / (f"plans_{torch.cuda.get_device_name(self.device).replace(' ', '_')}_{lib_hash}_"
+                                     f"h{cfg.hidden}_f{cfg.ffn}_v{cfg.vocab}_l{cfg.num_layers}_tp{self.tp_size}_"
+                                     f"t{self.max_tokens}_s{self.max_seqs}.json")
+            if key.exists():
+                rows = json.loads(key.read_text())
+                buf = (C.c_int32 * (4 * len(rows)))(*[x for r in rows for x in r])
+                _lib.check(self.lib.ag_model_set_gemm_plans(self.handle, buf, len(rows)))
+                return
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.ag_model_autotune(self.handle, torch.cuda.current_stream(self.device).cuda_stream))
+        if key is not None:
+            buf = (C.c_int32 * (4 * 512))()
+            n = int(self.lib.ag_model_get_gemm_plans(self.handle, buf, 512))
+            key.parent.mkdir(parents=True, exist_ok=True)
+            key.write_text(json.dumps([[buf[4 * i + j] for j in range(4)] for i in range(min(n, 512))]))
 
     def gemm_plans(self) -> list[tuple[str, int, int, int]]:
         kinds = ("qkv", "out", "fc1", "fc2", "lm_head")

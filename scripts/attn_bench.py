@@ -6,6 +6,7 @@ algorithmic FLOPs/bytes per SURVEY §8d: FLOPs = sum 4*H*(q*p + q(q+1)/2), bytes
 """
 import json
 import math
+import os
 import sys
 
 import torch
@@ -77,6 +78,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 2:  # extra cases recorded from real batches (scripts/make_attn_cases.py)
         import json as _j
         CASES.update({k: [tuple(x) for x in v] for k, v in _j.load(open(sys.argv[2])).items()})
+    only = os.environ.get("ATTN_CASES")  # comma-separated subset
     for name, seqs in CASES.items():
+        if only and name not in only.split(","):
+            continue
         r = run(seqs, HEADS)
         print(json.dumps({"case": name, "heads": HEADS, **r}), flush=True)

@@ -2,7 +2,9 @@
 # One GPU call: parity tests, smoke, a default bench line, the ncu launch list of the timed steps and
 # one --set full capture of the attention and GEMM kernels inside the timed region (AG_NCU_TIMED=1:
 # cudaProfilerStart/Stop around the K timed steps). Run under gpurun; everything lands in gpurun_out/.
-mkdir -p gpurun_out
+mkdir -p gpurun_out/plan_cache
+cp .plan_cache/* gpurun_out/plan_cache/ 2>/dev/null
+export AG_GEMM_PLAN_CACHE=gpurun_out/plan_cache  # autotune once per library build (bench/ncu runs reuse it)
 TAG=${TAG:-r1}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 nproc > gpurun_out/${TAG}_nproc.txt; lscpu | head -20 >> gpurun_out/${TAG}_nproc.txt

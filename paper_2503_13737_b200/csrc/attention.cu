@@ -51,13 +51,11 @@ constexpr int kRowBarOff = 6 * kRowWarpBytes;                  // + 6 warps x kR
 constexpr int kRowSmem = kRowBarOff + 6 * kRowStages * 8;
 constexpr int kSmemBytes = 1024 + (kTileSmem > kRowSmem ? kTileSmem : kRowSmem);
 
-AG_DEVICE void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-AG_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-AG_DEVICE void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// 2^x on the SFU without the denormal range fix-up of exp2f (arguments here are <= 0).
+AG_DEVICE float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 AG_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -207,12 +205,12 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnTmaps& tm, const A
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float mnew = fmaxf(m, mx);
     const float mref = mnew == -INFINITY ? 0.f : mnew;
-    const float alpha = exp2f(m - mref);
+    const float alpha = ex2_ftz(m - mref);
     m = mnew;
     uint32_t pa[4];  // P as bf16x2 per n-tile (row 0 only)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float p0 = exp2f(sc[j][0] - mref), p1 = exp2f(sc[j][1] - mref);
+      const float p0 = ex2_ftz(sc[j][0] - mref), p1 = ex2_ftz(sc[j][1] - mref);
       lpart = lpart * (j == 0 ? alpha : 1.f) + p0 + p1;
       pa[j] = pack_bf16x2(p0, p1);
     }
@@ -391,19 +389,23 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->s_empty[sbuf]);
       const int kbase = it.kv_start + j * kTN;
-      const int lim = row_ok ? min(kv_end, qpos + 1) - kbase : 0;  // valid columns [0, lim)
+      // Only the tiles that cross a row's causal / range end need a mask (CTA-uniform test on
+      // row 0, the row with the earliest end); rows past q_rows are never stored.
+      if (kbase + kTN > min(kv_end, ctx + it.q_start + 1)) {
+        const int lim = row_ok ? min(kv_end, qpos + 1) - kbase : 0;  // valid columns [0, lim)
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = c < lim ? s[c] : -INFINITY;
+      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        s[c] = c < lim ? s[c] * kLog2e : -INFINITY;
-        mx = fmaxf(mx, s[c]);
-      }
+      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      mx *= kLog2e;  // scores stay raw; the log2(e) scale is folded into the exponent's FMA
       // Lazy rescale: a row whose running max grew by more than 2^8 rescales l and its O row
       // (after every earlier P.V finished).  tcgen05.ld/st are .sync.aligned, so the decision to
       // touch TMEM is warp-uniform; rows that did not grow scale by 1.
       const bool grow = mx > m_used + kRescaleThresh;
       if (__any_sync(0xffffffffu, grow)) {
-        const float alpha = grow ? exp2f(m_used - mx) : 1.0f;  // 0 on a row's first visit
+        const float alpha = grow ? ex2_ftz(m_used - mx) : 1.0f;  // 0 on a row's first visit
         if (__any_sync(0xffffffffu, grow && j > 0 && m_used != -INFINITY)) {
           mbar_wait(&bars->o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc_fence_after();
@@ -433,7 +435,8 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float e0 = exp2f(s[half * 64 + 2 * i] - mref), e1 = exp2f(s[half * 64 + 2 * i + 1] - mref);
+          const float e0 = ex2_ftz(fmaf(s[half * 64 + 2 * i], kLog2e, -mref));
+          const float e1 = ex2_ftz(fmaf(s[half * 64 + 2 * i + 1], kLog2e, -mref));
           rs += e0 + e1;
           pk[i] = pack_bf16x2(e0, e1);
         }
@@ -501,8 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int n_tile_ctas = n_tile_items * p.heads;
   if (static_cast<int>(blockIdx.x) < n_tile_ctas) {
-    const AttnItem it = items[blockIdx.x / p.heads];
-    tile_tc(p, tm, it, blockIdx.x % p.heads, smem);
+    // head-major: the q tiles / splits of one head run side by side and share its K/V in L2
+    const AttnItem it = items[blockIdx.x % n_tile_items];
+    tile_tc(p, tm, it, blockIdx.x / n_tile_items, smem);
     return;
   }
   const int warp = threadIdx.x >> 5;

@@ -99,3 +99,47 @@ def test_13b_shape_mixed_batch_two_layers():
     print(f"13B-shape mixed step: S_f={b.num_tokens} max|dlogit|={d:.4g} agreement={agree:.3f}")
     assert d <= 5e-2
     assert agree >= 0.95
+
+
+def _prompt_batch(pool, cfg, rid, tok_rid, start, n):
+    """One sequence's chunk [start, start+n) with the token ids of request `tok_rid` (so two
+    requests can carry the same prompt)."""
+    from paper_2503_13737_b200.engine import DeviceBatch, synthetic_tokens
+    d = pool.demand_prompt_chunk(rid, n) if (n > 1 or not pool.is_resident(rid)) else pool.demand_tg(rid)
+    pool.allocate(rid, d)
+    p = np.arange(start, start + n, dtype=np.int32)
+    bt = np.asarray([pool.block_table(rid)], np.int32)
+    return DeviceBatch([rid], synthetic_tokens(tok_rid, p, cfg.vocab), p, np.asarray([0, n], np.int32),
+                       np.asarray([start], np.int32), bt, np.asarray(pool.slots(rid, start, n), np.int32),
+                       np.asarray([n - 1], np.int32), [rid])
+
+
+def test_long_context_100k_chunk_invariance():
+    """Config-4 regime on one GPU (2 OPT-13B-shaped layers): a 100k-token prompt prefilled in
+    16384-token chunks and, as a second request with the same tokens, in 12000-token chunks, then
+    one decode each.  Chunked prefill must not change the result (SURVEY §7 property): last-chunk
+    and decode logits agree within the bf16 tolerance and pick the same greedy token.  Exercises
+    split-KV tile attention over ~3k-page block tables and the extended position table."""
+    from paper_2503_13737_b200.executor import CudaExecutor
+    from paper_2503_13737_b200.kvc import BlockPool
+    P = 100_000
+    cfg = M.OPTConfig("opt-13b-2l-100k", hidden=5120, num_layers=2, num_heads=40, ffn=20480,
+                      max_positions=P + 64)
+    w = M.init_weights(cfg, seed=3, device="cuda", init="test")
+    pool = BlockPool(2 * (P // 32 + 8))
+    dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=16384, max_seqs=8, weights=w, parity_logits=True)
+    outs = []
+    for rid, chunk in ((0, 16384), (1, 12000)):
+        res = None
+        for start in range(0, P, chunk):
+            res = dev.execute(_prompt_batch(pool, cfg, rid, 0, start, min(chunk, P - start)))
+        dec = dev.execute(_prompt_batch(pool, cfg, rid, 0, P, 1))
+        outs.append((res.logits[:1].float().clone(), res.token_ids.copy(), dec.logits[:1].float().clone(),
+                     dec.token_ids.copy()))
+    (la, ta, da, tda), (lb, tb, db, tdb) = outs
+    d_last = (la - lb).abs().max().item()
+    d_dec = (da - db).abs().max().item()
+    print(f"100k prompt: max|dlogit| last-chunk {d_last:.4g}, decode {d_dec:.4g}")
+    assert torch.isfinite(la).all() and torch.isfinite(da).all()
+    assert d_last <= LOGIT_TOL and d_dec <= LOGIT_TOL
+    assert ta[0] == tb[0] and tda[0] == tdb[0]

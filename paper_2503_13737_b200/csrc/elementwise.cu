@@ -129,6 +129,86 @@ __global__ void __launch_bounds__(kLNThreads)
   }
 }
 
+// Warp-per-row LayerNorm for hidden <= 32 * 8 * kLNWarpVec (5120): the row lives in registers
+// (kLNWarpVec 16-B vectors per lane, all loads in flight at once), statistics are warp shuffles, and
+// there is no block barrier -- a 5120-wide LN of a few hundred rows is one latency round trip.
+constexpr int kLNWarpVec = 20;
+constexpr int kLNWarpsPerBlock = 8;
+
+__global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
+    layernorm_warp_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                          const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
+                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
+                          float eps, int rows, int hidden, __nv_bfloat16* __restrict__ out) {
+  const int r = blockIdx.x * kLNWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int src = row_index ? row_index[r] : r;
+  __nv_bfloat16* xr = x + static_cast<int64_t>(src) * hidden;
+  const int nvec = hidden / 8;
+  float vals[kLNWarpVec][8];
+  float sum = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i) {
+    const int idx = lane + i * 32;
+    if (idx < nvec) bf16x8_to_f32(*reinterpret_cast<const uint4*>(xr + idx * 8), vals[i]);
+  }
+  if (delta != nullptr) {
+#pragma unroll
+    for (int i = 0; i < kLNWarpVec; ++i) {
+      const int idx = lane + i * 32;
+      if (idx < nvec) {
+        float d[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta + static_cast<int64_t>(src) * hidden + idx * 8), d);
+        if (delta_bias != nullptr) {
+          float bb[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta_bias + idx * 8), bb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d[j] += bb[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vals[i][j] += d[j];
+        const uint4 packed = f32_to_bf16x8(vals[i]);
+        *reinterpret_cast<uint4*>(xr + idx * 8) = packed;  // updated residual stream
+        bf16x8_to_f32(packed, vals[i]);                    // normalise the rounded value
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i)
+    if (lane + i * 32 < nvec)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += vals[i][j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / hidden;
+  float sq = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i)
+    if (lane + i * 32 < nvec)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float c = vals[i][j] - mean;
+        sq += c * c;
+      }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / hidden + eps);
+  __nv_bfloat16* orow = out + static_cast<int64_t>(r) * hidden;
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i) {
+    const int idx = lane + i * 32;
+    if (idx < nvec) {
+      float g[8], b[8], y[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(gamma) + idx), g);
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(beta) + idx), b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] = (vals[i][j] - mean) * rstd * g[j] + b[j];
+      *reinterpret_cast<uint4*>(orow + idx * 8) = f32_to_bf16x8(y);
+    }
+  }
+}
+
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                                  int ld_src, const int32_t* __restrict__ slot_mapping, int rows, int heads,
                                  int head_dim, int block_size, __nv_bfloat16* __restrict__ kcache,
@@ -268,6 +348,11 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const
                              float eps, int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (hidden % 8 != 0 || hidden / 8 > kLNThreads * kLNMaxVec) return cudaErrorInvalidValue;
+  if (hidden / 8 <= 32 * kLNWarpVec) {
+    layernorm_warp_kernel<<<(rows + kLNWarpsPerBlock - 1) / kLNWarpsPerBlock, kLNWarpsPerBlock * 32, 0, stream>>>(
+        x, delta, delta_bias, row_index, gamma, beta, eps, rows, hidden, out);
+    return cudaGetLastError();
+  }
   layernorm_kernel<<<rows, kLNThreads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
                                                     out);
   return cudaGetLastError();

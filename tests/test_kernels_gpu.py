@@ -85,8 +85,8 @@ def test_gemm_epilogue_bias_residual_relu_f32(K, bn, splits):
     assert (out32.cpu() - ref32).abs().max().item() <= 1e-3 * ref32.abs().max().item() + 1e-4
 
 
-def test_layernorm_plain_delta_gather(K):
-    rows, H = 37, 5120
+@pytest.mark.parametrize("rows,H", [(37, 5120), (300, 256), (9, 12288)])  # warp-per-row / block kernels
+def test_layernorm_plain_delta_gather(K, rows, H):
     x, d, db = _bf((rows, H), 7), _bf((rows, H), 8), _bf((H,), 9)
     g, b = (1 + 0.1 * _bf((H,), 10).float()).to(torch.bfloat16), _bf((H,), 11)
     out = K.layernorm(x.to(DEV), g.to(DEV), b.to(DEV))

@@ -205,6 +205,8 @@ def run_ours(args):
         batches.append(b)
         return orig_exec(b)
     ex.execute = recording_exec
+    peaks = load_peaks()
+    ex.set_roofline_peaks(peaks["tensor_sustained"], peaks["hbm"])
     ex.set_profiling(True)
     launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
     sampler = ClockSampler(local)
@@ -246,6 +248,7 @@ def run_ours(args):
     g_ms = sum(prof_k[c]["ms"] for c in gemm_cls)
     g_fl = sum(prof_k[c]["flops"] for c in gemm_cls)
     g_n = sum(prof_k[c]["launches"] for c in gemm_cls)
+    g_roof = sum(prof_k[c]["roofline_ms"] for c in gemm_cls)
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
     prof_total_ms = sum(v["ms"] for v in prof_k.values())
     shares = {k: round(v["ms"] / prof_total_ms, 4) for k, v in prof_k.items() if prof_total_ms > 0 and v["ms"] > 0}
@@ -258,10 +261,14 @@ def run_ours(args):
         "gemm": {"bound": "tensor", "kernel": "tcgen05 GEMM (QKV/out/FC1/FC2/LM head)", "achieved": achieved,
                  "peak": peaks["tensor_sustained"], "unit": "TFLOP/s",
                  "frac": achieved / peaks["tensor_sustained"] if achieved else None,
+                 # per launch max(FLOPs/tensor peak, weight+activation bytes/HBM peak): small-M
+                 # launches are weight-streaming bound, so this is the fraction of each launch's own roofline
+                 "frac_of_per_launch_roofline": g_roof / g_ms if g_ms else None,
                  "peak_source": peaks["source"] + " bf16 sustained", "traffic": None, "launches": g_n,
                  "share": g_ms / prof_total_ms if prof_total_ms else None,
                  "per_launch_ms": g_ms / g_n if g_n else None, "per_launch_flops": g_fl / g_n if g_n else None},
         "attention": {"bound": "hbm", "kernel": "mixed paged attention (tcgen05 tiles + streaming decode rows)",
+                      "frac_of_per_launch_roofline": attn["roofline_ms"] / attn["ms"] if attn["ms"] else None,
                       "achieved": attn["bytes"] / (attn["ms"] / 1e3) / 1e9 if attn["ms"] else 0.0,
                       "peak": peaks["hbm"], "unit": "GB/s",
                       "frac": (attn["bytes"] / (attn["ms"] / 1e3) / 1e9 / peaks["hbm"]) if attn["ms"] else None,

@@ -145,6 +145,11 @@ AG_API int32_t ag_model_set_gemm_plans(ag_model* m, const int32_t* rows4, int32_
  * get_profile fills up to n entries per class: summed ms, algorithmic FLOPs and HBM bytes, launches. */
 AG_API int32_t ag_model_set_profiling(ag_model* m, int32_t on);
 AG_API int32_t ag_model_get_profile(ag_model* m, double* ms, double* flops, double* bytes, int64_t* counts, int32_t n);
+/* Roofline accounting: with peaks set, every profiled launch adds
+ * max(FLOPs / tensor peak, algorithmic bytes / HBM peak) to its class; get_roofline_ms returns the
+ * per-class sums, so sum(roofline) / sum(measured) is the class's fraction of its roofline. */
+AG_API int32_t ag_model_set_roofline_peaks(ag_model* m, double tensor_tflops, double hbm_gbs);
+AG_API int32_t ag_model_get_roofline_ms(ag_model* m, double* roof_ms, int32_t n);
 /* Kernel launches issued by the last forward (ours only; NCCL calls counted as AG_K_ALLREDUCE). */
 AG_API int64_t ag_model_last_launches(ag_model* m);
 /* Bytes of packed metadata (BatchPlan arrays + attention work list) copied H2D by the last step. */

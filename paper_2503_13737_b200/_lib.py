@@ -22,6 +22,7 @@ PROF_CLASSES = ("embed", "layernorm", "qkv_gemm", "attention", "out_gemm", "fc1_
 i32 = C.c_int32
 i64 = C.c_int64
 f32 = C.c_float
+f64 = C.c_double
 vp = C.c_void_p
 P_i32 = C.POINTER(C.c_int32)
 P_f32 = C.POINTER(C.c_float)
@@ -61,6 +62,8 @@ _SIGS = {
     "ag_model_forward_staged": (i32, [vp, vp, vp, vp]),
     "ag_model_set_profiling": (i32, [vp, i32]),
     "ag_model_get_profile": (i32, [vp, vp, vp, vp, vp, i32]),
+    "ag_model_set_roofline_peaks": (i32, [vp, f64, f64]),
+    "ag_model_get_roofline_ms": (i32, [vp, vp, i32]),
     "ag_model_last_launches": (i64, [vp]),
     "ag_model_autotune": (i32, [vp, vp]),
     "ag_model_get_gemm_plans": (i32, [vp, vp, i32]),

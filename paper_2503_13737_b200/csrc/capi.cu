@@ -242,6 +242,9 @@ struct ag_model {
   double prof_flops[AG_PROF_CLASSES] = {};
   double prof_bytes[AG_PROF_CLASSES] = {};
   int64_t prof_count[AG_PROF_CLASSES] = {};
+  // per-launch roofline time max(FLOPs / tensor peak, bytes / HBM peak), summed per class
+  double prof_roof_ms[AG_PROF_CLASSES] = {};
+  double peak_tflops = 0.0, peak_gbs = 0.0;
   int64_t launches_last = 0;
   int64_t h2d_last = 0;
   int64_t launches_total = 0;
@@ -339,6 +342,8 @@ void prof_harvest(ag_model* m) {
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, m->prof_events[r.ev], m->prof_events[r.ev + 1]) == cudaSuccess) {
       m->prof_ms[r.cls] += ms;
+      if (m->peak_tflops > 0.0 && m->peak_gbs > 0.0)
+        m->prof_roof_ms[r.cls] += 1e3 * std::max(r.flops / (m->peak_tflops * 1e12), r.bytes / (m->peak_gbs * 1e9));
       m->prof_flops[r.cls] += r.flops;
       m->prof_bytes[r.cls] += r.bytes;
       m->prof_count[r.cls] += 1;
@@ -807,7 +812,7 @@ int32_t ag_model_set_profiling(ag_model* m, int32_t on) {
   m->prof_on = on != 0;
   m->prof_pending.clear();
   for (int i = 0; i < AG_PROF_CLASSES; ++i) {
-    m->prof_ms[i] = m->prof_flops[i] = m->prof_bytes[i] = 0.0;
+    m->prof_ms[i] = m->prof_flops[i] = m->prof_bytes[i] = m->prof_roof_ms[i] = 0.0;
     m->prof_count[i] = 0;
   }
   if (m->prof_on && m->prof_events.empty()) {
@@ -825,6 +830,19 @@ int32_t ag_model_get_profile(ag_model* m, double* ms, double* flops, double* byt
     if (bytes) bytes[i] = m->prof_bytes[i];
     if (counts) counts[i] = m->prof_count[i];
   }
+  return AG_OK;
+}
+
+int32_t ag_model_set_roofline_peaks(ag_model* m, double tensor_tflops, double hbm_gbs) {
+  if (!m || tensor_tflops < 0.0 || hbm_gbs < 0.0) return fail(AG_EINVAL, "bad peaks");
+  m->peak_tflops = tensor_tflops;
+  m->peak_gbs = hbm_gbs;
+  return AG_OK;
+}
+
+int32_t ag_model_get_roofline_ms(ag_model* m, double* roof_ms, int32_t n) {
+  if (!m || !roof_ms) return fail(AG_EINVAL, "null argument");
+  for (int i = 0; i < std::min<int>(n, AG_PROF_CLASSES); ++i) roof_ms[i] = m->prof_roof_ms[i];
   return AG_OK;
 }
 

@@ -36,37 +36,45 @@ struct GemmCfg {
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256;
 };
 
-AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const uint32_t (&r)[32]) {
-  float v[32];
+// Store W (a multiple of 8) consecutive bf16 values v[0..W) at dst.
+template <int W>
+AG_DEVICE void store_bf16(__nv_bfloat16* dst, const float* v) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  for (int q = 0; q < W / 8; ++q)
+    st_global_v4(dst + q * 8, pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]),
+                 pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]));
+}
 
-  if (ep.bias != nullptr) {
-    const uint4* b4 = reinterpret_cast<const uint4*>(ep.bias + col0);
+// v[0..W) += W consecutive bf16 values at src.
+template <int W>
+AG_DEVICE void add_bf16(float* v, const __nv_bfloat16* src) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w = __ldg(b4 + q);
-      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  for (int q = 0; q < W / 8; ++q) {
+    const uint4 w = s4[q];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        float2 f = unpack_bf16x2(ws[h]);
-        v[q * 8 + h * 2] += f.x;
-        v[q * 8 + h * 2 + 1] += f.y;
-      }
+    for (int h = 0; h < 4; ++h) {
+      const float2 f = unpack_bf16x2(ws[h]);
+      v[q * 8 + h * 2] += f.x;
+      v[q * 8 + h * 2 + 1] += f.y;
     }
   }
+}
 
+// Fused epilogue of W consecutive accumulator columns [col0, col0 + W) of one output row: bias,
+// then either the QKV split (q scaled -> q buffer; K/V -> their paged cache slots) or residual
+// add / ReLU -> bf16 or f32 output.  W = 32 (one TMEM load per thread) or 8 (split-K reduce); a
+// W-column group never straddles a head (head_dim % 32 == 0).
+template <int W>
+AG_DEVICE void epilogue_cols(const GemmEpilogue& ep, int row, int col0, float* v) {
+  if (ep.bias != nullptr) add_bf16<W>(v, ep.bias + col0);
   if (ep.mode == kEpiQkv) {
     const int region = col0 / ep.hq;  // 0 = q, 1 = k, 2 = v
     if (region == 0) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= ep.q_scale;
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldc + col0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        st_global_v4(dst + q * 8, pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]),
-                     pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]), pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]),
-                     pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]));
+      for (int j = 0; j < W; ++j) v[j] *= ep.q_scale;
+      store_bf16<W>(reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldc + col0, v);
       return;
     }
     const int slot = ep.slot_mapping[row];
@@ -77,48 +85,30 @@ AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const u
     const int blk = slot / ep.block_size;
     const int off = slot - blk * ep.block_size;
     __nv_bfloat16* cache = (region == 1) ? ep.kcache : ep.vcache;
-    __nv_bfloat16* dst =
-        cache + (((size_t)blk * ep.heads + head) * ep.block_size + off) * ep.head_dim + d;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      st_global_v4(dst + q * 8, pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]),
-                   pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]), pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]),
-                   pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]));
+    store_bf16<W>(cache + (((size_t)blk * ep.heads + head) * ep.block_size + off) * ep.head_dim + d, v);
     return;
   }
-
-  if (ep.residual != nullptr) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(ep.residual + (size_t)row * ep.ldr + col0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w = r4[q];
-      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        float2 f = unpack_bf16x2(ws[h]);
-        v[q * 8 + h * 2] += f.x;
-        v[q * 8 + h * 2 + 1] += f.y;
-      }
-    }
-  }
+  if (ep.residual != nullptr) add_bf16<W>(v, ep.residual + (size_t)row * ep.ldr + col0);
   if (ep.relu) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+    for (int j = 0; j < W; ++j) v[j] = fmaxf(v[j], 0.0f);
   }
   if (ep.out_f32) {
     float* dst = reinterpret_cast<float*>(ep.out) + (size_t)row * ep.ldc + col0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < W / 4; ++q)
       st_global_v4(dst + q * 4, __float_as_uint(v[q * 4]), __float_as_uint(v[q * 4 + 1]),
                    __float_as_uint(v[q * 4 + 2]), __float_as_uint(v[q * 4 + 3]));
   } else {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldc + col0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      st_global_v4(dst + q * 8, pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]),
-                   pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]), pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]),
-                   pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]));
+    store_bf16<W>(reinterpret_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldc + col0, v);
   }
+}
+
+AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  epilogue_cols<32>(ep, row, col0, v);
 }
 
 template <int BN, int AM>
@@ -447,33 +437,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-// Sum the K-split fp32 partials of 32 consecutive columns and apply the fused epilogue.
+// Sum the K-split fp32 partials of 8 consecutive columns per thread and apply the fused epilogue
+// (consecutive threads on consecutive 32-B column groups of a row: coalesced, 2 x splits loads in
+// flight per thread).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M,
                                                             int N, GemmEpilogue ep) {
-  const int chunks = N / 32;
-  const int64_t total = static_cast<int64_t>(M) * chunks;
+  const int groups = N / 8;
+  const int64_t total = static_cast<int64_t>(M) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int row = static_cast<int>(i / chunks);
-    const int col0 = static_cast<int>(i - static_cast<int64_t>(row) * chunks) * 32;
-    float acc[32];
+    const int row = static_cast<int>(i / groups);
+    const int col0 = static_cast<int>(i - static_cast<int64_t>(row) * groups) * 8;
+    float acc[8];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    const float* src = partial + (size_t)row * N + col0;
+#pragma unroll 4
     for (int s = 0; s < splits; ++s) {
-      const float4* src = reinterpret_cast<const float4*>(partial + ((size_t)s * M + row) * N + col0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = src[q];
-        acc[q * 4] += v.x;
-        acc[q * 4 + 1] += v.y;
-        acc[q * 4 + 2] += v.z;
-        acc[q * 4 + 3] += v.w;
-      }
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(src + (size_t)s * M * N));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(src + (size_t)s * M * N) + 1);
+      acc[0] += a.x;
+      acc[1] += a.y;
+      acc[2] += a.z;
+      acc[3] += a.w;
+      acc[4] += b.x;
+      acc[5] += b.y;
+      acc[6] += b.z;
+      acc[7] += b.w;
     }
-    uint32_t r[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[j]);
-    epilogue_chunk(ep, row, col0, r);
+    epilogue_cols<8>(ep, row, col0, acc);
   }
 }
 
@@ -540,8 +532,8 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   gemm_bf16_tn_kernel<BN, AM><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1) return e;
-  const int64_t work = static_cast<int64_t>(M) * (N / 32);
-  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+  const int64_t work = static_cast<int64_t>(M) * (N / 8);
+  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
   splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
   return cudaGetLastError();
 }
@@ -565,8 +557,8 @@ static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   gemm2_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1) return e;
-  const int64_t work = static_cast<int64_t>(M) * (N / 32);
-  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 8));
+  const int64_t work = static_cast<int64_t>(M) * (N / 8);
+  int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
   splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
   return cudaGetLastError();
 }

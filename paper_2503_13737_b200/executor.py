@@ -89,12 +89,16 @@ class CudaExecutor:
     def set_profiling(self, on: bool) -> None:
         _lib.check(self.lib.ag_model_set_profiling(self.handle, int(on)))
 
+    def set_roofline_peaks(self, tensor_tflops: float, hbm_gbs: float) -> None:
+        _lib.check(self.lib.ag_model_set_roofline_peaks(self.handle, float(tensor_tflops), float(hbm_gbs)))
+
     def profile(self) -> dict:
         n = len(_lib.PROF_CLASSES)
-        ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+        ms, fl, by, roof = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
         cnt = (C.c_int64 * n)()
         _lib.check(self.lib.ag_model_get_profile(self.handle, ms, fl, by, cnt, n))
-        return {name: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
+        _lib.check(self.lib.ag_model_get_roofline_ms(self.handle, roof, n))
+        return {name: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i], "roofline_ms": roof[i]}
                 for i, name in enumerate(_lib.PROF_CLASSES)}
 
     def _autotune(self) -> None:

@@ -176,6 +176,13 @@ AG_API int32_t ag_paged_attention(const void* q, int32_t ldq, const void* k_pool
 AG_API int32_t ag_layernorm(void* x, const void* delta, const void* delta_bias, const int32_t* row_index,
                      const void* gamma, const void* beta, float eps, int32_t rows, int32_t hidden, void* out,
                      void* stream);
+/* Llama-family variants (north_star kernel list; not on the OPT path, which uses LayerNorm and
+ * learned positions): RMSNorm with optional in-place residual add, and rotary embedding in place
+ * (rotate-half convention over the first rotary_dim dims of each head, angle pos * theta^(-2i/d)). */
+AG_API int32_t ag_rmsnorm(void* x, const void* delta, const void* gamma, float eps, int32_t rows, int32_t hidden,
+                   void* out, void* stream);
+AG_API int32_t ag_rope(void* x, int32_t ld, const int32_t* positions, int32_t rows, int32_t heads, int32_t head_dim,
+                int32_t rotary_dim, float theta, void* stream);
 AG_API int32_t ag_embed_pos(const int32_t* ids, const int32_t* positions, const void* tok_emb, const void* pos_emb,
                      int32_t pos_offset, int32_t rows, int32_t hidden, int32_t vocab, int32_t pos_rows,
                      void* out, void* stream);

@@ -53,6 +53,26 @@ def layernorm(x, g, b, eps=1e-5):
     return rb((x - mean) * torch.rsqrt(var + eps) * f32(g) + f32(b))
 
 
+def rmsnorm(x, g, eps=1e-6):
+    """Llama RMSNorm (transformers LlamaRMSNorm: fp32 statistics, weight applied after)."""
+    return rb(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * f32(g))
+
+
+def rope(x, positions, heads, head_dim=128, rotary_dim=None, theta=10000.0):
+    """Rotate-half rotary embedding (transformers apply_rotary_pos_emb with rotate_half) on
+    x [rows, heads*head_dim] fp32; the first rotary_dim dims of each head rotate."""
+    rd = rotary_dim or head_dim
+    half = rd // 2
+    inv_freq = theta ** (-torch.arange(0, half, dtype=torch.float64) * 2.0 / rd)
+    ang = positions.double()[:, None] * inv_freq[None, :]
+    cos, sin = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+    y = x.clone().view(x.shape[0], heads, head_dim)
+    x1, x2 = y[..., :half].clone(), y[..., half:rd].clone()
+    y[..., :half] = x1 * cos - x2 * sin
+    y[..., half:rd] = x2 * cos + x1 * sin
+    return rb(y.view(x.shape[0], heads * head_dim))
+
+
 def paged_attention(q, k_pool, v_pool, block_table, cu_q, ctx_len, block_size=32):
     """q [S, heads*128] (already scaled); pools [blocks, heads, bs, 128]; returns fp32 [S, heads*128].
 

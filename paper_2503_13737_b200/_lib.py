@@ -74,6 +74,8 @@ _SIGS = {
     "ag_kv_append": (i32, [vp, vp, i32, vp, i32, i32, i32, vp, vp, vp]),
     "ag_paged_attention": (i32, [vp, i32, vp, vp, i32, vp, i32, vp, vp, vp, vp, i32, i32, i32, vp, i32, vp, i64, vp]),
     "ag_layernorm": (i32, [vp, vp, vp, vp, vp, vp, f32, i32, i32, vp, vp]),
+    "ag_rmsnorm": (i32, [vp, vp, vp, f32, i32, i32, vp, vp]),
+    "ag_rope": (i32, [vp, i32, vp, i32, i32, i32, i32, f32, vp]),
     "ag_embed_pos": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, vp]),
     "ag_argmax": (i32, [vp, i32, i32, i32, i32, vp, vp, vp]),
     "ag_kv_swap_out": (i32, [vp, vp, i32, i64, vp, vp]),

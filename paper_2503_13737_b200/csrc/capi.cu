@@ -1115,6 +1115,25 @@ int32_t ag_layernorm(void* x, const void* delta, const void* delta_bias, const i
   return AG_OK;
 }
 
+int32_t ag_rmsnorm(void* x, const void* delta, const void* gamma, float eps, int32_t rows, int32_t hidden, void* out,
+                   void* stream) {
+  if (!x || !gamma || !out) return fail(AG_EINVAL, "null pointer");
+  if (hidden % 8 || hidden > 5120) return fail(AG_EINVAL, "hidden must be a multiple of 8 and <= 5120");
+  AG_CUDA(ag::launch_rmsnorm(static_cast<bf16*>(x), static_cast<const bf16*>(delta), static_cast<const bf16*>(gamma),
+                             eps, rows, hidden, static_cast<bf16*>(out), static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
+int32_t ag_rope(void* x, int32_t ld, const int32_t* positions, int32_t rows, int32_t heads, int32_t head_dim,
+                int32_t rotary_dim, float theta, void* stream) {
+  if (!x || !positions) return fail(AG_EINVAL, "null pointer");
+  if (rotary_dim % 8 || rotary_dim > head_dim || ld % 4 || head_dim % 4 || theta <= 1.0f)
+    return fail(AG_EINVAL, "rotary_dim must be a multiple of 8 <= head_dim, theta > 1");
+  AG_CUDA(ag::launch_rope(static_cast<bf16*>(x), ld, positions, rows, heads, head_dim, rotary_dim, theta,
+                          static_cast<cudaStream_t>(stream)));
+  return AG_OK;
+}
+
 int32_t ag_embed_pos(const int32_t* ids, const int32_t* positions, const void* tok_emb, const void* pos_emb,
                      int32_t pos_offset, int32_t rows, int32_t hidden, int32_t vocab, int32_t pos_rows, void* out,
                      void* stream) {

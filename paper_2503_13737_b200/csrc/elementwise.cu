@@ -209,6 +209,95 @@ __global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
   }
 }
 
+// RMSNorm (Llama-family variants of the served model): warp per row, optional in-place residual add.
+//   x[r] += delta[r] (rounded to bf16, written back);  out[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * gamma
+__global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
+    rmsnorm_warp_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                        const __nv_bfloat16* __restrict__ gamma, float eps, int rows, int hidden,
+                        __nv_bfloat16* __restrict__ out) {
+  const int r = blockIdx.x * kLNWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  __nv_bfloat16* xr = x + static_cast<int64_t>(r) * hidden;
+  const int nvec = hidden / 8;
+  float vals[kLNWarpVec][8];
+  float sq = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i) {
+    const int idx = lane + i * 32;
+    if (idx < nvec) {
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(xr + idx * 8), vals[i]);
+      if (delta != nullptr) {
+        float d[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta + static_cast<int64_t>(r) * hidden + idx * 8), d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vals[i][j] += d[j];
+        const uint4 packed = f32_to_bf16x8(vals[i]);
+        *reinterpret_cast<uint4*>(xr + idx * 8) = packed;
+        bf16x8_to_f32(packed, vals[i]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sq += vals[i][j] * vals[i][j];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / hidden + eps);
+  __nv_bfloat16* orow = out + static_cast<int64_t>(r) * hidden;
+#pragma unroll
+  for (int i = 0; i < kLNWarpVec; ++i) {
+    const int idx = lane + i * 32;
+    if (idx < nvec) {
+      float g[8], y[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(gamma) + idx), g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] = vals[i][j] * rstd * g[j];
+      *reinterpret_cast<uint4*>(orow + idx * 8) = f32_to_bf16x8(y);
+    }
+  }
+}
+
+// Rotary position embedding, in place on [rows, heads * head_dim] bf16 (q or k), rotate-half
+// (GPT-NeoX / Llama) convention over the first rotary_dim dims of every head:
+//   (x1, x2) <- (x1 cos - x2 sin, x2 cos + x1 sin),  angle = pos * theta^(-2i / rotary_dim).
+// One thread per (row, head, pair of 2 x 4 dims): 8-B vector loads/stores of both halves.
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ x, int ld, const int32_t* __restrict__ positions, int rows,
+                            int heads, int head_dim, int rotary_dim, float log2_theta) {
+  const int half = rotary_dim / 2;
+  const int quads = half / 4;
+  const int64_t total = static_cast<int64_t>(rows) * heads * quads;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int q4 = static_cast<int>(t % quads);
+    const int64_t rh = t / quads;
+    const int h = static_cast<int>(rh % heads);
+    const int r = static_cast<int>(rh / heads);
+    const float pos = static_cast<float>(positions[r]);
+    __nv_bfloat16* base = x + static_cast<int64_t>(r) * ld + static_cast<int64_t>(h) * head_dim;
+    uint2 a = *reinterpret_cast<const uint2*>(base + q4 * 4);
+    uint2 b = *reinterpret_cast<const uint2*>(base + half + q4 * 4);
+    float x1[4], x2[4];
+    float2 f;
+    f = unpack_bf16x2(a.x); x1[0] = f.x; x1[1] = f.y;
+    f = unpack_bf16x2(a.y); x1[2] = f.x; x1[3] = f.y;
+    f = unpack_bf16x2(b.x); x2[0] = f.x; x2[1] = f.y;
+    f = unpack_bf16x2(b.y); x2[2] = f.x; x2[3] = f.y;
+    float y1[4], y2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = q4 * 4 + j;
+      const float inv_freq = exp2f(-log2_theta * (2.0f * i) / rotary_dim);
+      float sn, cs;
+      sincosf(pos * inv_freq, &sn, &cs);
+      y1[j] = x1[j] * cs - x2[j] * sn;
+      y2[j] = x2[j] * cs + x1[j] * sn;
+    }
+    *reinterpret_cast<uint2*>(base + q4 * 4) = make_uint2(pack_bf16x2(y1[0], y1[1]), pack_bf16x2(y1[2], y1[3]));
+    *reinterpret_cast<uint2*>(base + half + q4 * 4) =
+        make_uint2(pack_bf16x2(y2[0], y2[1]), pack_bf16x2(y2[2], y2[3]));
+  }
+}
+
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                                  int ld_src, const int32_t* __restrict__ slot_mapping, int rows, int heads,
                                  int head_dim, int block_size, __nv_bfloat16* __restrict__ kcache,
@@ -355,6 +444,26 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const
   }
   layernorm_kernel<<<rows, kLNThreads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
                                                     out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const __nv_bfloat16* gamma, float eps,
+                           int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (hidden % 8 != 0 || hidden / 8 > 32 * kLNWarpVec) return cudaErrorInvalidValue;
+  rmsnorm_warp_kernel<<<(rows + kLNWarpsPerBlock - 1) / kLNWarpsPerBlock, kLNWarpsPerBlock * 32, 0, stream>>>(
+      x, delta, gamma, eps, rows, hidden, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rope(__nv_bfloat16* x, int ld, const int32_t* positions, int rows, int heads, int head_dim,
+                        int rotary_dim, float theta, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (rotary_dim % 8 != 0 || rotary_dim > head_dim || ld % 4 != 0 || head_dim % 4 != 0 || theta <= 1.0f)
+    return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(rows) * heads * (rotary_dim / 8);
+  rope_kernel<<<grid_for(work, 256), 256, 0, stream>>>(x, ld, positions, rows, heads, head_dim, rotary_dim,
+                                                        log2f(theta));
   return cudaGetLastError();
 }
 

@@ -61,6 +61,14 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta,
                              const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps,
                              int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream);
 
+// RMSNorm over rows (hidden <= 5120), optional in-place residual add x += delta first.
+cudaError_t launch_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const __nv_bfloat16* gamma, float eps,
+                           int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream);
+
+// Rotary embedding in place on [rows, heads*head_dim] (rotate-half convention, first rotary_dim dims).
+cudaError_t launch_rope(__nv_bfloat16* x, int ld, const int32_t* positions, int rows, int heads, int head_dim,
+                        int rotary_dim, float theta, cudaStream_t stream);
+
 // standalone paged KV append: k/v rows [rows, heads*head_dim] -> cache slots
 cudaError_t launch_kv_append(const __nv_bfloat16* k, const __nv_bfloat16* v, int ld_src,
                              const int32_t* slot_mapping, int rows, int heads, int head_dim,

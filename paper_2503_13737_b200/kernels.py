@@ -104,6 +104,24 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
     return out
 
 
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6, delta: torch.Tensor | None = None) -> torch.Tensor:
+    """RMSNorm over rows; with delta, x += delta in place first (residual stream)."""
+    _need_cuda(x, gamma, delta)
+    out = torch.empty_like(x)
+    _lib.check(_lib.load().ag_rmsnorm(x.data_ptr(), _ptr(delta), gamma.data_ptr(), eps, x.shape[0], x.shape[1],
+                                      out.data_ptr(), _stream()))
+    return out
+
+
+def rope(x: torch.Tensor, positions: torch.Tensor, heads: int, head_dim: int = 128, rotary_dim: int | None = None,
+         theta: float = 10000.0) -> torch.Tensor:
+    """Rotary embedding in place on x [rows, heads*head_dim] (rotate-half convention); returns x."""
+    _need_cuda(x, positions)
+    _lib.check(_lib.load().ag_rope(x.data_ptr(), x.stride(0), positions.data_ptr(), x.shape[0], heads, head_dim,
+                                   rotary_dim or head_dim, theta, _stream()))
+    return x
+
+
 def embed_pos(ids: torch.Tensor, positions: torch.Tensor, tok_emb: torch.Tensor, pos_emb: torch.Tensor,
               pos_offset: int = 2) -> torch.Tensor:
     _need_cuda(ids, positions, tok_emb, pos_emb)

@@ -102,6 +102,30 @@ def test_layernorm_plain_delta_gather(K, rows, H):
     assert (out3.float().cpu() - orc.layernorm(x.float()[idx.long()], g, b)).abs().max().item() <= 3e-2
 
 
+@pytest.mark.parametrize("rows,H", [(33, 5120), (7, 4096), (200, 256)])
+def test_rmsnorm(K, rows, H):
+    x, d = _bf((rows, H), 41), _bf((rows, H), 42)
+    g = (1 + 0.1 * _bf((H,), 43).float()).to(torch.bfloat16)
+    out = K.rmsnorm(x.to(DEV), g.to(DEV))
+    assert (out.float().cpu() - orc.rmsnorm(x.float(), g)).abs().max().item() <= 3e-2
+    xd = x.to(DEV)
+    out2 = K.rmsnorm(xd, g.to(DEV), delta=d.to(DEV))
+    xn = orc.rb(x.float() + d.float())
+    assert torch.equal(xd.float().cpu(), xn)
+    assert (out2.float().cpu() - orc.rmsnorm(xn, g)).abs().max().item() <= 3e-2
+
+
+@pytest.mark.parametrize("rows,heads,rd", [(57, 4, 128), (5, 32, 64), (300, 2, 128)])
+def test_rope(K, rows, heads, rd):
+    x = _bf((rows, heads * 128), 44)
+    pos = torch.randint(0, 16384, (rows,), dtype=torch.int32)
+    out = K.rope(x.to(DEV).clone(), pos.to(DEV), heads, 128, rd)
+    ref = orc.rope(x.float(), pos, heads, 128, rd)
+    # fp32 angle (pos * inv_freq, as transformers computes it) vs the fp64 oracle: <= 4e-3 rad at
+    # pos < 16384, then bf16 rounding of the output
+    assert (out.float().cpu() - ref).abs().max().item() <= 3e-2
+
+
 def test_embed_bit_exact(K):
     V, H, P = 1000, 256, 300
     te, pe = _bf((V, H), 12), _bf((P, H), 13)

@@ -129,81 +129,82 @@ __global__ void __launch_bounds__(kLNThreads)
   }
 }
 
-// Warp-per-row LayerNorm for hidden <= 32 * 8 * kLNWarpVec (5120): the row lives in registers
-// (kLNWarpVec 16-B vectors per lane, all loads in flight at once), statistics are warp shuffles, and
-// there is no block barrier -- a 5120-wide LN of a few hundred rows is one latency round trip.
-constexpr int kLNWarpVec = 20;
+// Row-per-block LayerNorm with 2 vectors (16 values) per thread: hidden/16 threads (320 for OPT-13B)
+// so the whole row is one load round trip and the per-thread work is tiny; two block reductions
+// (warp shuffles + one smem exchange each).  For hidden <= 16384.
+constexpr int kLNVpt = 2;
+constexpr int kLNWarpVec = 20;  // RMSNorm warp-per-row capacity (hidden <= 5120)
 constexpr int kLNWarpsPerBlock = 8;
 
-__global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
-    layernorm_warp_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
-                          const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
-                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
-                          float eps, int rows, int hidden, __nv_bfloat16* __restrict__ out) {
-  const int r = blockIdx.x * kLNWarpsPerBlock + (threadIdx.x >> 5);
-  if (r >= rows) return;
-  const int lane = threadIdx.x & 31;
+AG_DEVICE float block_sum_dyn(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.0f;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(1024)
+    layernorm_row_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                         const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
+                         const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
+                         float eps, int hidden, __nv_bfloat16* __restrict__ out) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
   __nv_bfloat16* xr = x + static_cast<int64_t>(src) * hidden;
   const int nvec = hidden / 8;
-  float vals[kLNWarpVec][8];
+  float v[kLNVpt][8];
   float sum = 0.0f;
 #pragma unroll
-  for (int i = 0; i < kLNWarpVec; ++i) {
-    const int idx = lane + i * 32;
-    if (idx < nvec) bf16x8_to_f32(*reinterpret_cast<const uint4*>(xr + idx * 8), vals[i]);
-  }
-  if (delta != nullptr) {
-#pragma unroll
-    for (int i = 0; i < kLNWarpVec; ++i) {
-      const int idx = lane + i * 32;
-      if (idx < nvec) {
+  for (int i = 0; i < kLNVpt; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
+    if (idx < nvec) {
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(xr + idx * 8), v[i]);
+      if (delta != nullptr) {
         float d[8];
         bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta + static_cast<int64_t>(src) * hidden + idx * 8), d);
         if (delta_bias != nullptr) {
           float bb[8];
-          bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta_bias + idx * 8), bb);
+          bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(delta_bias) + idx), bb);
 #pragma unroll
           for (int j = 0; j < 8; ++j) d[j] += bb[j];
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) vals[i][j] += d[j];
-        const uint4 packed = f32_to_bf16x8(vals[i]);
+        for (int j = 0; j < 8; ++j) v[i][j] += d[j];
+        const uint4 packed = f32_to_bf16x8(v[i]);
         *reinterpret_cast<uint4*>(xr + idx * 8) = packed;  // updated residual stream
-        bf16x8_to_f32(packed, vals[i]);                    // normalise the rounded value
+        bf16x8_to_f32(packed, v[i]);                       // normalise the rounded value
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += v[i][j];
     }
   }
-#pragma unroll
-  for (int i = 0; i < kLNWarpVec; ++i)
-    if (lane + i * 32 < nvec)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sum += vals[i][j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float mean = sum / hidden;
+  const float mean = block_sum_dyn(sum, red) / hidden;
   float sq = 0.0f;
 #pragma unroll
-  for (int i = 0; i < kLNWarpVec; ++i)
-    if (lane + i * 32 < nvec)
+  for (int i = 0; i < kLNVpt; ++i)
+    if (threadIdx.x + i * blockDim.x < nvec)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float c = vals[i][j] - mean;
+        const float c = v[i][j] - mean;
         sq += c * c;
       }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  const float rstd = rsqrtf(sq / hidden + eps);
+  const float rstd = rsqrtf(block_sum_dyn(sq, red) / hidden + eps);
   __nv_bfloat16* orow = out + static_cast<int64_t>(r) * hidden;
 #pragma unroll
-  for (int i = 0; i < kLNWarpVec; ++i) {
-    const int idx = lane + i * 32;
+  for (int i = 0; i < kLNVpt; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
     if (idx < nvec) {
       float g[8], b[8], y[8];
       bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(gamma) + idx), g);
       bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(beta) + idx), b);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) y[j] = (vals[i][j] - mean) * rstd * g[j] + b[j];
+      for (int j = 0; j < 8; ++j) y[j] = (v[i][j] - mean) * rstd * g[j] + b[j];
       *reinterpret_cast<uint4*>(orow + idx * 8) = f32_to_bf16x8(y);
     }
   }
@@ -437,9 +438,10 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const
                              float eps, int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (hidden % 8 != 0 || hidden / 8 > kLNThreads * kLNMaxVec) return cudaErrorInvalidValue;
-  if (hidden / 8 <= 32 * kLNWarpVec) {
-    layernorm_warp_kernel<<<(rows + kLNWarpsPerBlock - 1) / kLNWarpsPerBlock, kLNWarpsPerBlock * 32, 0, stream>>>(
-        x, delta, delta_bias, row_index, gamma, beta, eps, rows, hidden, out);
+  if (hidden / 8 <= 1024 * kLNVpt) {
+    const int threads = ((hidden / 8 + kLNVpt - 1) / kLNVpt + 31) / 32 * 32;
+    layernorm_row_kernel<<<rows, threads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
+                                                       out);
     return cudaGetLastError();
   }
   layernorm_kernel<<<rows, kLNThreads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,

@@ -210,6 +210,7 @@ struct ag_model {
   float *part_o = nullptr, *part_ml = nullptr;
   int part_cap = 0;
   float* splitk_ws = nullptr;
+  float* acc32 = nullptr;  // fp32 [T, H] split-K accumulator of out-proj / FC2 at TP=1 (zero between uses)
   int64_t splitk_cap = 0;
   GemmTable tune;
   // metadata: one pinned host buffer mirrored by one device buffer
@@ -277,10 +278,32 @@ int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char*
 
 // GEMM against a weight: (N tile, K splits) from the autotuned table for this M bucket (or the
 // analytic planner before autotune), then launch with the matching tensor map.
+ag::GemmPlan pick_plan(const WeightMap& w, int M, int N, int K, int64_t splitk_cap, const GemmTable* tune, int kind) {
+  ag::GemmPlan p{0, 0, 128};
+  if (tune && tune->ready && kind >= 0) {
+    for (size_t i = 0; i < tune->m_bucket.size(); ++i) {
+      if (M <= tune->m_bucket[i] || i + 1 == tune->m_bucket.size()) {
+        p = tune->plan[kind][i];
+        break;
+      }
+    }
+    if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
+    if (p.am < 128 && M > p.am) p.am = 128;
+  }
+  if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_cap);
+  if (p.bn == 256 && !w.has256 && p.am != 256) p.bn = 128;
+  return p;
+}
+
 cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
                    cudaStream_t s, float* splitk_ws, int64_t splitk_cap, const GemmTable* tune = nullptr,
-                   int kind = -1) {
+                   int kind = -1, const ag::GemmPlan* forced = nullptr) {
   ag::GemmPlan p{0, 0, 128};
+  if (forced) {
+    p = *forced;
+    if (p.am == 256) return ag::launch_gemm(a.box(128), w.box(p.bn / 2), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, 256);
+    return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
+  }
   if (tune && tune->ready && kind >= 0) {
     for (size_t i = 0; i < tune->m_bucket.size(); ++i) {
       if (M <= tune->m_bucket[i] || i + 1 == tune->m_bucket.size()) {
@@ -431,6 +454,9 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   chk(dmalloc(&m->part_ml, static_cast<size_t>(m->part_cap) * m->heads_l * 2));
   m->splitk_cap = int64_t(32) << 20;  // fp32 K-split partials (128 MB)
   chk(dmalloc(&m->splitk_ws, static_cast<size_t>(m->splitk_cap)));
+  chk(dmalloc(&m->acc32, T * c.hidden));
+  if (r == AG_OK && cudaMemset(m->acc32, 0, sizeof(float) * T * c.hidden) != cudaSuccess)
+    r = fail(AG_ECUDA, "memset acc32");
   // metadata capacity: token arrays, sequence arrays, block table, attention work list
   const size_t max_items = static_cast<size_t>(c.max_tokens) + c.max_seqs + 64 * static_cast<size_t>(ag::num_sms());
   m->meta_cap = align_up(4 * sizeof(int32_t) * T, 256) + align_up(2 * sizeof(int32_t) * (c.max_seqs + 1), 256) +
@@ -465,7 +491,7 @@ void ag_model_destroy(ag_model* m) {
   if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
   void* dev[] = {m->resid, m->xln, m->qbuf, m->attn, m->ffn, m->proj, m->lm_in, m->logits, m->cand_val,
                  m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev,
-                 m->splitk_ws};
+                 m->splitk_ws, m->acc32};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (m->meta_host) cudaFreeHost(m->meta_host);
@@ -636,19 +662,32 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
   const double bf = 2.0;
   m->launches_last = 0;
   const double ln_bytes = bf * 2.0 * S * H;
+  bool final_acc = false;
   if (S > 0) {
     {
       ProfScope ps(m, AG_K_EMBED, s, 0.0, bf * 3.0 * S * H);
       AG_CUDA(ag::launch_embed(m->d_ids, m->d_pos, m->tok_emb, m->pos_emb, 2, S, H, c.vocab, c.pos_rows, m->resid, s));
     }
     const float qscale = 1.0f / std::sqrt(static_cast<float>(m->head_dim));
+    // TP=1: an out-proj / FC2 plan that splits K accumulates into acc32 with fp32 reductions and the
+    // next LayerNorm applies bias + residual (no reduce launch); else the GEMM epilogue does it
+    auto atomic_plan = [&](const WeightMap& wm, int N, int K, int kind, ag::GemmPlan& p) {
+      p = pick_plan(wm, S, N, K, m->splitk_cap, &m->tune, kind);
+      return !tp && p.k_splits > 1;
+    };
+    bool acc_pending = false;
     for (int l = 0; l < c.num_layers; ++l) {
       const LayerState& L = m->layers[l];
       const ag_layer_weights& w = L.w;
       {
         // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
-        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, (tp && l > 0) ? 2.0 * ln_bytes : ln_bytes);
-        if (tp && l > 0) {
+        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ((tp || acc_pending) && l > 0) ? 2.0 * ln_bytes : ln_bytes);
+        if (acc_pending) {  // previous layer's FC2 was split-K into acc32: finish its epilogue here
+          AG_CUDA(ag::launch_layernorm_acc(m->resid, m->acc32, static_cast<const bf16*>(m->layers[l - 1].w.fc2_b),
+                                           nullptr, static_cast<const bf16*>(w.ln1_g), static_cast<const bf16*>(w.ln1_b),
+                                           c.ln_eps, S, H, m->xln, s));
+          acc_pending = false;
+        } else if (tp && l > 0) {
           AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(m->layers[l - 1].w.fc2_b), nullptr,
                                        static_cast<const bf16*>(w.ln1_g), static_cast<const bf16*>(w.ln1_b), c.ln_eps,
                                        S, H, m->xln, s));
@@ -705,7 +744,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
         ag::GemmEpilogue eo;
         eo.ldc = H;
-        if (!tp) {
+        ag::GemmPlan po;
+        const bool out_atomic = atomic_plan(L.tm_out, H, m->hq, kGemmOut, po);
+        if (out_atomic) {
+          eo.mode = ag::kEpiAtomicF32;
+          eo.acc32 = m->acc32;
+        } else if (!tp) {
           eo.bias = static_cast<const bf16*>(w.out_b);
           eo.residual = m->resid;
           eo.ldr = H;
@@ -714,7 +758,9 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           eo.out = m->proj;
         }
         ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmOut));
+        AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmOut,
+                       &po));
+        acc_pending = out_atomic;
         AG_TRY(dbg(s, "out_gemm", l));
       }
       if (tp) {
@@ -726,6 +772,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(w.out_b), nullptr,
                                      static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps, S,
                                      H, m->xln, s));
+      } else if (acc_pending) {
+        ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, 2.0 * ln_bytes);
+        AG_CUDA(ag::launch_layernorm_acc(m->resid, m->acc32, static_cast<const bf16*>(w.out_b), nullptr,
+                                         static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps,
+                                         S, H, m->xln, s));
+        acc_pending = false;
       } else {
         ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ln_bytes);
         AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln2_g),
@@ -744,7 +796,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
       {
         ag::GemmEpilogue e2;
         e2.ldc = H;
-        if (!tp) {
+        ag::GemmPlan p2;
+        const bool fc2_atomic = atomic_plan(L.tm_fc2, H, m->ffn_l, kGemmFc2, p2);
+        if (fc2_atomic) {
+          e2.mode = ag::kEpiAtomicF32;
+          e2.acc32 = m->acc32;
+        } else if (!tp) {
           e2.bias = static_cast<const bf16*>(w.fc2_b);
           e2.residual = m->resid;
           e2.ldr = H;
@@ -753,13 +810,20 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
           e2.out = m->proj;
         }
         ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
-        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc2));
+        AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc2,
+                       &p2));
+        acc_pending = fc2_atomic;
         AG_TRY(dbg(s, "fc2_gemm", l));
       }
       if (tp) {
         ProfScope ps(m, AG_K_ALLREDUCE, s, 0.0, bf * S * H);
         AG_TRY(allreduce_bf16(m, m->proj, static_cast<size_t>(S) * H, s));
       }
+    }
+    if (acc_pending) {
+      // last FC2 split K into acc32: the final LayerNorm (logit rows) applies bias + residual to the
+      // rows it reads; every row of acc32 is re-zeroed for the next step
+      final_acc = true;
     }
     if (tp) {  // fold the last FC2 all-reduce into the residual stream
       const ag_layer_weights& wl = m->layers[c.num_layers - 1].w;
@@ -773,8 +837,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     {
       // final LayerNorm only on the rows that emit a token (logit skip)
       ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, bf * 2.0 * NL * H);
-      AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H,
-                                   m->lm_in, s));
+      if (final_acc)
+        AG_CUDA(ag::launch_layernorm_acc(m->resid, m->acc32, static_cast<const bf16*>(m->layers[c.num_layers - 1].w.fc2_b),
+                                         m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H, m->lm_in, s));
+      else
+        AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, m->d_lrows, m->final_g, m->final_b, c.ln_eps, NL, H,
+                                     m->lm_in, s));
     }
     ag::GemmEpilogue el;
     el.out = logits_out ? static_cast<void*>(logits_out) : static_cast<void*>(m->logits);
@@ -803,6 +871,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
       AG_CUDA(ag::launch_argmax_merge(m->gathered_val, m->gathered_idx, c.tp_size, NL, out_tokens_dev, s));
     }
   }
+  if (final_acc) AG_CUDA(cudaMemsetAsync(m->acc32, 0, sizeof(float) * static_cast<size_t>(S) * H, s));
   m->launches_total += m->launches_last;
   return AG_OK;
 }
@@ -900,12 +969,16 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
     const Shape& sh = shapes[k];
     for (size_t b = 0; b < t.m_bucket.size(); ++b) {
       const int M = std::min(t.m_bucket[b], sh.mcap);
-      ag::GemmEpilogue ep;
-      ep.out = sh.out;
-      ep.ldc = sh.N;
-      ep.out_f32 = sh.out_f32;
       float best = 1e30f;
       for (const ag::GemmPlan& p : cands) {
+        ag::GemmEpilogue ep;
+        ep.out = sh.out;
+        ep.ldc = sh.N;
+        ep.out_f32 = sh.out_f32;
+        if (c.tp_size == 1 && (k == kGemmOut || k == kGemmFc2) && p.k_splits > 1) {
+          ep.mode = ag::kEpiAtomicF32;  // as the forward runs split-K out-proj / FC2 at TP=1
+          ep.acc32 = m->acc32;
+        }
         if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.am < 128 && M > p.am) continue;
@@ -935,6 +1008,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  AG_CUDA(cudaMemsetAsync(m->acc32, 0, sizeof(float) * T * H, s));
+  AG_CUDA(cudaStreamSynchronize(s));
   t.ready = true;
   return AG_OK;
 }

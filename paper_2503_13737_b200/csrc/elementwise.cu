@@ -148,8 +148,9 @@ AG_DEVICE float block_sum_dyn(float v, float* red) {
   return t;
 }
 
+template <typename DeltaT>
 __global__ void __launch_bounds__(1024)
-    layernorm_row_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+    layernorm_row_kernel(__nv_bfloat16* __restrict__ x, DeltaT* __restrict__ delta,
                          const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
                          float eps, int hidden, __nv_bfloat16* __restrict__ out) {
@@ -167,7 +168,15 @@ __global__ void __launch_bounds__(1024)
       bf16x8_to_f32(*reinterpret_cast<const uint4*>(xr + idx * 8), v[i]);
       if (delta != nullptr) {
         float d[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta + static_cast<int64_t>(src) * hidden + idx * 8), d);
+        if constexpr (sizeof(DeltaT) == 4) {  // fp32 split-K accumulator: read, then re-zero
+          float4* d4 = reinterpret_cast<float4*>(delta + static_cast<int64_t>(src) * hidden + idx * 8);
+          const float4 a = __ldcg(d4), b = __ldcg(d4 + 1);
+          d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w; d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+          d4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          d4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(delta + static_cast<int64_t>(src) * hidden + idx * 8), d);
+        }
         if (delta_bias != nullptr) {
           float bb[8];
           bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(delta_bias) + idx), bb);
@@ -440,12 +449,23 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const
   if (hidden % 8 != 0 || hidden / 8 > kLNThreads * kLNMaxVec) return cudaErrorInvalidValue;
   if (hidden / 8 <= 1024 * kLNVpt) {
     const int threads = ((hidden / 8 + kLNVpt - 1) / kLNVpt + 31) / 32 * 32;
-    layernorm_row_kernel<<<rows, threads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
-                                                       out);
+    layernorm_row_kernel<const __nv_bfloat16><<<rows, threads, 0, stream>>>(x, delta, delta_bias, row_index, gamma,
+                                                                           beta, eps, hidden, out);
     return cudaGetLastError();
   }
   layernorm_kernel<<<rows, kLNThreads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
                                                     out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm_acc(__nv_bfloat16* x, float* acc32, const __nv_bfloat16* delta_bias,
+                                 const int32_t* row_index, const __nv_bfloat16* gamma, const __nv_bfloat16* beta,
+                                 float eps, int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (hidden % 8 != 0 || hidden / 8 > 1024 * kLNVpt || acc32 == nullptr) return cudaErrorInvalidValue;
+  const int threads = ((hidden / 8 + kLNVpt - 1) / kLNVpt + 31) / 32 * 32;
+  layernorm_row_kernel<float><<<rows, threads, 0, stream>>>(x, acc32, delta_bias, row_index, gamma, beta, eps, hidden,
+                                                            out);
   return cudaGetLastError();
 }
 

@@ -104,7 +104,20 @@ AG_DEVICE void epilogue_cols(const GemmEpilogue& ep, int row, int col0, float* v
   }
 }
 
+AG_DEVICE void red_add_v4(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const uint32_t (&r)[32]) {
+  if (ep.mode == kEpiAtomicF32) {
+    float* dst = ep.acc32 + (size_t)row * ep.ldc + col0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      red_add_v4(dst + q * 4, __uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]), __uint_as_float(r[q * 4 + 2]),
+                 __uint_as_float(r[q * 4 + 3]));
+    return;
+  }
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int col0 = n_blk * BN + c * 32;
         if (row < M && col0 < N) {
-          if (k_splits == 1) {
+          if (k_splits == 1 || ep.mode == kEpiAtomicF32) {
             epilogue_chunk(ep, row, col0, r);
           } else {  // fp32 partial of this K split; splitk_reduce_kernel applies the epilogue
             float* dst = partial + ((size_t)ks * M + row) * N + col0;
@@ -412,7 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int col0 = n_blk * BN + c * 32;
         if (row < M && col0 < N) {
-          if (k_splits == 1) {
+          if (k_splits == 1 || ep.mode == kEpiAtomicF32) {
             epilogue_chunk(ep, row, col0, r);
           } else {
             float* dst = partial + ((size_t)ks * M + row) * N + col0;
@@ -531,7 +544,7 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   if (units < grid) grid = units;
   gemm_bf16_tn_kernel<BN, AM><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || k_splits == 1) return e;
+  if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
   splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
@@ -556,7 +569,7 @@ static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   if (2 * units < grid) grid = 2 * units;
   gemm2_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || k_splits == 1) return e;
+  if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
   splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
@@ -568,12 +581,12 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
                         int am) {
   if (M <= 0) return cudaSuccess;
   if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
-    if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
+    if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
     if (bn == 256) return launch_bn2<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 128) return launch_bn2<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     return cudaErrorInvalidValue;
   }
-  if (k_splits > 1 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
+  if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
   if (am != 128 && M > am) return cudaErrorInvalidValue;  // small-M variant needs one m-block
   if (am == 32) {
     if (bn == 256) return launch_bn<256, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);

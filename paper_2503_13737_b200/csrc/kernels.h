@@ -8,7 +8,10 @@
 
 namespace ag {
 
-enum EpiMode : int { kEpiPlain = 0, kEpiQkv = 1 };
+// kEpiAtomicF32: every K split adds its fp32 tile into acc32 (red.global.add.v4.f32, no bias /
+// residual / conversion here); the consumer (layernorm with an fp32 delta) finishes the epilogue
+// and re-zeroes acc32.  Lets out-proj / FC2 split K across all SMs with no reduce launch.
+enum EpiMode : int { kEpiPlain = 0, kEpiQkv = 1, kEpiAtomicF32 = 2 };
 
 struct GemmEpilogue {
   int mode = kEpiPlain;
@@ -28,6 +31,7 @@ struct GemmEpilogue {
   int heads = 0;
   int head_dim = 128;
   int block_size = 32;
+  float* acc32 = nullptr;  // [M, ldc] fp32 (kEpiAtomicF32)
 };
 
 int make_tmap_kmajor(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld_elems,
@@ -60,6 +64,12 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta,
                              const __nv_bfloat16* delta_bias, const int32_t* row_index,
                              const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps,
                              int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream);
+
+// Same, with the residual delta in fp32 (a kEpiAtomicF32 GEMM's accumulator) plus bias: x[src] =
+// bf16(x[src] + acc32[src] + bias) for the normalised rows; acc32 rows read are zeroed again.
+cudaError_t launch_layernorm_acc(__nv_bfloat16* x, float* acc32, const __nv_bfloat16* delta_bias,
+                                 const int32_t* row_index, const __nv_bfloat16* gamma, const __nv_bfloat16* beta,
+                                 float eps, int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream);
 
 // RMSNorm over rows (hidden <= 5120), optional in-place residual add x += delta first.
 cudaError_t launch_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const __nv_bfloat16* gamma, float eps,

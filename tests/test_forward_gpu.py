@@ -143,3 +143,36 @@ def test_long_context_100k_chunk_invariance():
     assert torch.isfinite(la).all() and torch.isfinite(da).all()
     assert d_last <= LOGIT_TOL and d_dec <= LOGIT_TOL
     assert ta[0] == tb[0] and tda[0] == tdb[0]
+
+
+@pytest.mark.parametrize("splits", [2, 5])
+def test_split_k_atomic_epilogue_forward(splits):
+    """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32 and the
+    next LayerNorm finishes bias + residual (and re-zeroes acc32).  Forced on for every M bucket via
+    the plan table; two consecutive mixed steps vs the oracle (acc32 must be clean between steps)."""
+    import ctypes as C
+    from paper_2503_13737_b200.executor import CudaExecutor
+    from paper_2503_13737_b200.kvc import BlockPool
+    cfg = M.OPTConfig("opt-13b-2l", hidden=5120, num_layers=2, num_heads=40, ffn=20480, max_positions=4096)
+    w = M.init_weights(cfg, seed=5, init="test")
+    pool = BlockPool(1024)
+    dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=1024, max_seqs=64, weights=w, parity_logits=True)
+    rows = []
+    for kind, mb, bn, ks, am in dev.gemm_plans():
+        kid = ("qkv", "out", "fc1", "fc2", "lm_head").index(kind)
+        if kind in ("out", "fc2"):
+            bn, ks, am = 128, splits, 128
+        rows.append([kid, mb, bn, ks + 100 * am])
+    buf = (C.c_int32 * (4 * len(rows)))(*[x for r in rows for x in r])
+    from paper_2503_13737_b200 import _lib
+    _lib.check(dev.lib.ag_model_set_gemm_plans(dev.handle, buf, len(rows)))
+    ref = OracleExecutor(cfg, w, pool.total_blocks)
+    worst = 0.0
+    for segs in ([(0, 0, 700), (1, 0, 60)], [(0, 700, 1), (1, 60, 200), (2, 0, 33)]):
+        b = _make_batch(pool, cfg, segs)
+        a, r = dev.execute(b), ref.execute(b)
+        n = len(b.logit_rows)
+        worst = max(worst, (a.logits[:n] - r.logits[:n]).abs().max().item())
+        assert np.array_equal(a.token_ids[:n], r.token_ids[:n])
+    print(f"split-K {splits} atomic epilogue: max|dlogit|={worst:.4g}")
+    assert worst <= 5e-2

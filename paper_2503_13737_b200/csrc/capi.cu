@@ -287,7 +287,7 @@ ag::GemmPlan pick_plan(const WeightMap& w, int M, int N, int K, int64_t splitk_c
         break;
       }
     }
-    if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
+    if (p.k_splits != ag::kStreamK && static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
     if (p.am < 128 && M > p.am) p.am = 128;
   }
   if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_cap);
@@ -961,6 +961,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
                                   ag::GemmPlan{64, 4}, ag::GemmPlan{256, 6}, ag::GemmPlan{128, 6},
                                   ag::GemmPlan{256, 8}, ag::GemmPlan{128, 8}})
       cands.push_back({q.bn, q.k_splits, am});
+  for (int am : {128, 64, 32})  // stream-K (atomic fp32 epilogue: out-proj / FC2 at TP=1 only)
+    for (int bn : {256, 128, 64}) cands.push_back({bn, ag::kStreamK, am});
   cudaEvent_t e0, e1;
   AG_CUDA(cudaEventCreate(&e0));
   AG_CUDA(cudaEventCreate(&e1));
@@ -982,9 +984,13 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.am < 128 && M > p.am) continue;
-        const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
-        if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
-        if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
+        if (p.k_splits == ag::kStreamK) {
+          if (c.tp_size != 1 || (k != kGemmOut && k != kGemmFc2) || p.am == 256) continue;
+        } else {
+          const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
+          if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
+          if (static_cast<int64_t>(p.k_splits) * M * sh.N > m->splitk_cap) continue;
+        }
         const int wbox = p.am == 256 ? p.bn / 2 : p.bn;
         const CUtensorMap& am = sh.a->box(p.am == 256 ? 128 : p.am);
         const int nw = static_cast<int>(sh.w.size());

@@ -124,6 +124,52 @@ AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const u
   epilogue_cols<32>(ep, row, col0, v);
 }
 
+// Work decomposition shared by the three warp roles of the 1-CTA kernel.  Classic: unit t =
+// (m_blk, k_split, n_blk), m fastest (concurrent CTAs share a weight tile), strided over CTAs.
+// Stream-K (k_splits == kStreamK): CTA c takes the contiguous k-block range [c*U/G, (c+1)*U/G)
+// of the flattened (n_blk, m_blk, kb) space, U = tiles x k-blocks, cut at tile boundaries into
+// segments; every CTA streams the same number of weight k-blocks (no wave quantisation), and
+// partial tiles meet in the atomic fp32 epilogue (kEpiAtomicF32 only).
+struct SegIter {
+  int num_m, num_kb, k_splits, kb_per, num_tiles, t;
+  long long u, u_end;
+  bool streamk;
+  AG_DEVICE SegIter(int M, int N, int K, int bm, int bn, int ks) {
+    num_m = (M + bm - 1) / bm;
+    const int num_n = (N + bn - 1) / bn;
+    num_kb = (K + kBK - 1) / kBK;
+    streamk = ks == kStreamK;
+    k_splits = streamk ? 1 : ks;
+    kb_per = (num_kb + k_splits - 1) / k_splits;
+    num_tiles = num_m * num_n * k_splits;
+    t = blockIdx.x;
+    const long long U = static_cast<long long>(num_m) * num_n * num_kb;
+    u = U * blockIdx.x / gridDim.x;
+    u_end = U * (blockIdx.x + 1) / gridDim.x;
+  }
+  AG_DEVICE bool next(int& m_blk, int& n_blk, int& ks_idx, int& kb0, int& kb1) {
+    if (streamk) {
+      if (u >= u_end) return false;
+      const long long tile = u / num_kb;
+      kb0 = static_cast<int>(u - tile * num_kb);
+      kb1 = static_cast<int>(min(static_cast<long long>(num_kb), kb0 + (u_end - u)));
+      m_blk = static_cast<int>(tile % num_m);
+      n_blk = static_cast<int>(tile / num_m);
+      ks_idx = 0;
+      u += kb1 - kb0;
+      return true;
+    }
+    if (t >= num_tiles) return false;
+    m_blk = t % num_m;
+    ks_idx = (t / num_m) % k_splits;
+    n_blk = t / (num_m * k_splits);
+    kb0 = ks_idx * kb_per;
+    kb1 = min(num_kb, kb0 + kb_per);
+    t += gridDim.x;
+    return true;
+  }
+};
+
 template <int BN, int AM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -144,11 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_m = (M + kBM - 1) / kBM;
-  const int num_n = (N + BN - 1) / BN;
-  const int num_kb_total = (K + kBK - 1) / kBK;
-  const int kb_per = (num_kb_total + k_splits - 1) / k_splits;
-  // work unit = (m_blk, k_split, n_blk) with m fastest so CTAs running together share weights
-  const int num_tiles = num_m * num_n * k_splits;
+  int m_blk, n_blk, ks, kb0, kb1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -178,12 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_w = num_m <= 2 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_blk = t % num_m;
-        const int ks = (t / num_m) % k_splits;
-        const int n_blk = t / (num_m * k_splits);
-        const int kb0 = ks * kb_per;
-        const int kb1 = min(num_kb_total, kb0 + kb_per);
+      SegIter it(M, N, K, kBM, BN, k_splits);
+      while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
@@ -205,13 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      SegIter it(M, N, K, kBM, BN, k_splits);
+      while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int ks = (t / num_m) % k_splits;
-        const int kb0 = ks * kb_per;
-        const int kb1 = min(num_kb_total, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -238,10 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m_blk = t % num_m;
-      const int ks = (t / num_m) % k_splits;
-      const int n_blk = t / (num_m * k_splits);
+    SegIter it(M, N, K, kBM, BN, k_splits);
+    while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * kBM + ew * 32 + lane;
@@ -538,10 +572,12 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int units = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * k_splits;
+  if (k_splits == kStreamK && ep.mode != kEpiAtomicF32) return cudaErrorInvalidValue;
+  const int64_t tiles = static_cast<int64_t>((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int64_t units = k_splits == kStreamK ? tiles * ((K + kBK - 1) / kBK) : tiles * k_splits;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (units < grid) grid = units;
+  if (units < grid) grid = static_cast<int>(units);
   gemm_bf16_tn_kernel<BN, AM><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
@@ -581,6 +617,7 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
                         int am) {
   if (M <= 0) return cudaSuccess;
   if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
+    if (k_splits == kStreamK) return cudaErrorInvalidValue;
     if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
     if (bn == 256) return launch_bn2<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 128) return launch_bn2<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);

@@ -46,6 +46,8 @@ int pick_block_n(int M, int N);
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int bn,
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits = 1,
                         float* partial = nullptr, int am = 128);
+// k_splits == kStreamK: stream-K over all SMs (1-CTA kernel, kEpiAtomicF32 epilogue only).
+constexpr int kStreamK = 99;
 struct GemmPlan {
   int bn;
   int k_splits;

@@ -145,7 +145,7 @@ def test_long_context_100k_chunk_invariance():
     assert ta[0] == tb[0] and tda[0] == tdb[0]
 
 
-@pytest.mark.parametrize("splits", [2, 5])
+@pytest.mark.parametrize("splits", [2, 5, 99])  # 99 = stream-K (kStreamK)
 def test_split_k_atomic_epilogue_forward(splits):
     """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32 and the
     next LayerNorm finishes bias + residual (and re-zeroes acc32).  Forced on for every M bucket via

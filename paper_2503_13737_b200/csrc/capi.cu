@@ -211,6 +211,9 @@ struct ag_model {
   int part_cap = 0;
   float* splitk_ws = nullptr;
   float* acc32 = nullptr;  // fp32 [T, H] split-K accumulator of out-proj / FC2 at TP=1 (zero between uses)
+  float* acc_big = nullptr;  // fp32 [T, max(3*hq, ffn)] stream-K accumulator of QKV / FC1 (zero between uses)
+  int64_t acc_big_cols = 0;
+  bool deterministic = false;  // AG_DETERMINISTIC=1: no fp32 atomics (split-K via the reduce kernel)
   int64_t splitk_cap = 0;
   GemmTable tune;
   // metadata: one pinned host buffer mirrored by one device buffer
@@ -318,6 +321,20 @@ cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, con
   if (p.bn == 256 && !w.has256 && p.am != 256) p.bn = 128;
   if (p.am == 256) return ag::launch_gemm(a.box(128), w.box(p.bn / 2), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, 256);
   return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
+}
+
+// QKV / FC1: a stream-K plan accumulates atomically into acc_big, then the finish kernel applies the
+// real epilogue (bias, q scale + paged KV scatter, ReLU) and re-zeroes the accumulator.
+cudaError_t gemm_planned(const ActMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
+                         const ag::GemmPlan& p, cudaStream_t s, float* splitk_ws, int64_t splitk_cap, float* acc_big) {
+  if (p.k_splits != ag::kStreamK) return gemm_w(a, w, M, N, K, ep, s, splitk_ws, splitk_cap, nullptr, -1, &p);
+  ag::GemmEpilogue ea;
+  ea.mode = ag::kEpiAtomicF32;
+  ea.acc32 = acc_big;
+  ea.ldc = N;
+  cudaError_t e = gemm_w(a, w, M, N, K, ea, s, splitk_ws, splitk_cap, nullptr, -1, &p);
+  if (e != cudaSuccess) return e;
+  return ag::launch_splitk_finish(acc_big, M, N, ep, s);
 }
 
 int32_t amap(ActMap* a, const void* ptr, int64_t rows, int64_t k, const char* what) {
@@ -455,6 +472,14 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   m->splitk_cap = int64_t(32) << 20;  // fp32 K-split partials (128 MB)
   chk(dmalloc(&m->splitk_ws, static_cast<size_t>(m->splitk_cap)));
   chk(dmalloc(&m->acc32, T * c.hidden));
+  m->acc_big_cols = std::max(3 * m->hq, m->ffn_l);
+  {
+    const char* e = std::getenv("AG_DETERMINISTIC");
+    m->deterministic = e && e[0] == '1';
+  }
+  chk(dmalloc(&m->acc_big, T * m->acc_big_cols));
+  if (r == AG_OK && cudaMemset(m->acc_big, 0, sizeof(float) * T * m->acc_big_cols) != cudaSuccess)
+    r = fail(AG_ECUDA, "memset acc_big");
   if (r == AG_OK && cudaMemset(m->acc32, 0, sizeof(float) * T * c.hidden) != cudaSuccess)
     r = fail(AG_ECUDA, "memset acc32");
   // metadata capacity: token arrays, sequence arrays, block table, attention work list
@@ -491,7 +516,7 @@ void ag_model_destroy(ag_model* m) {
   if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
   void* dev[] = {m->resid, m->xln, m->qbuf, m->attn, m->ffn, m->proj, m->lm_in, m->logits, m->cand_val,
                  m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev,
-                 m->splitk_ws, m->acc32};
+                 m->splitk_ws, m->acc32, m->acc_big};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (m->meta_host) cudaFreeHost(m->meta_host);
@@ -673,7 +698,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     // next LayerNorm applies bias + residual (no reduce launch); else the GEMM epilogue does it
     auto atomic_plan = [&](const WeightMap& wm, int N, int K, int kind, ag::GemmPlan& p) {
       p = pick_plan(wm, S, N, K, m->splitk_cap, &m->tune, kind);
-      return !tp && p.k_splits > 1;
+      if (m->deterministic && p.k_splits == ag::kStreamK) p.k_splits = 1;
+      return !tp && p.k_splits > 1 && !m->deterministic;
     };
     bool acc_pending = false;
     for (int l = 0; l < c.num_layers; ++l) {
@@ -712,7 +738,9 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ep.head_dim = m->head_dim;
         ep.block_size = c.block_size;
         ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmQkv));
+        ag::GemmPlan pq = pick_plan(L.tm_qkv, S, 3 * m->hq, H, m->splitk_cap, &m->tune, kGemmQkv);
+        if (m->deterministic && pq.k_splits == ag::kStreamK) pq.k_splits = 1;
+        AG_CUDA(gemm_planned(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, pq, s, m->splitk_ws, m->splitk_cap, m->acc_big));
         AG_TRY(dbg(s, "qkv_gemm", l));
       }
       {
@@ -790,7 +818,9 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e1.out = m->ffn;
         e1.ldc = m->ffn_l;
         ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
-        AG_CUDA(gemm_w(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc1));
+        ag::GemmPlan p1 = pick_plan(L.tm_fc1, S, m->ffn_l, H, m->splitk_cap, &m->tune, kGemmFc1);
+        if (m->deterministic && p1.k_splits == ag::kStreamK) p1.k_splits = 1;
+        AG_CUDA(gemm_planned(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, p1, s, m->splitk_ws, m->splitk_cap, m->acc_big));
         AG_TRY(dbg(s, "fc1_gemm", l));
       }
       {
@@ -981,11 +1011,18 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
           ep.mode = ag::kEpiAtomicF32;  // as the forward runs split-K out-proj / FC2 at TP=1
           ep.acc32 = m->acc32;
         }
+        const bool finish = p.k_splits == ag::kStreamK && (k == kGemmQkv || k == kGemmFc1);
+        ag::GemmEpilogue ea;  // stream-K QKV / FC1: atomic accumulation, then the finish kernel
+        ea.mode = ag::kEpiAtomicF32;
+        ea.acc32 = m->acc_big;
+        ea.ldc = sh.N;
+        const ag::GemmEpilogue& eg = finish ? ea : ep;
         if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.am < 128 && M > p.am) continue;
         if (p.k_splits == ag::kStreamK) {
-          if (c.tp_size != 1 || (k != kGemmOut && k != kGemmFc2) || p.am == 256) continue;
+          if (p.am == 256 || k == kGemmLm) continue;
+          if ((k == kGemmOut || k == kGemmFc2) && c.tp_size != 1) continue;
         } else {
           const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;
           if ((nkb + per - 1) / per != p.k_splits || (p.k_splits > 1 && per < 2)) continue;
@@ -994,13 +1031,17 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         const int wbox = p.am == 256 ? p.bn / 2 : p.bn;
         const CUtensorMap& am = sh.a->box(p.am == 256 ? 128 : p.am);
         const int nw = static_cast<int>(sh.w.size());
-        AG_CUDA(ag::launch_gemm(am, sh.w[nw - 1]->box(wbox), M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits, m->splitk_ws,
+        AG_CUDA(ag::launch_gemm(am, sh.w[nw - 1]->box(wbox), M, sh.N, sh.K, p.bn, eg, 0, s, p.k_splits, m->splitk_ws,
                                 p.am));
+        if (finish) AG_CUDA(ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s));
         const int iters = 8;
         AG_CUDA(cudaEventRecord(e0, s));
         for (int rep = 0; rep < iters; ++rep)
-          AG_CUDA(ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, ep, 0, s, p.k_splits,
+        {
+          AG_CUDA(ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, eg, 0, s, p.k_splits,
                                   m->splitk_ws, p.am));
+          if (finish) AG_CUDA(ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s));
+        }
         AG_CUDA(cudaEventRecord(e1, s));
         AG_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;

@@ -516,6 +516,24 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   }
 }
 
+// Stream-K finish for GEMMs whose epilogue cannot be deferred to a consumer (QKV, FC1): the atomic
+// fp32 accumulator acc[M, N] gets the fused epilogue (8 columns per thread) and is re-zeroed.
+__global__ void __launch_bounds__(256) splitk_finish_kernel(float* __restrict__ acc, int M, int N, GemmEpilogue ep) {
+  const int groups = N / 8;
+  const int64_t total = static_cast<int64_t>(M) * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / groups);
+    const int col0 = static_cast<int>(i - static_cast<int64_t>(row) * groups) * 8;
+    float4* src = reinterpret_cast<float4*>(acc + (size_t)row * N + col0);
+    const float4 a = __ldcg(src), b = __ldcg(src + 1);
+    src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    epilogue_cols<8>(ep, row, col0, v);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
@@ -638,6 +656,15 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
   if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   if (bn == 64) return launch_bn<64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+}
+
+cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& ep, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (N % 8 != 0 || ep.mode == kEpiAtomicF32) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(M) * (N / 8);
+  const int g = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
+  splitk_finish_kernel<<<g, 256, 0, stream>>>(acc, M, N, ep);
+  return cudaGetLastError();
 }
 
 GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats) {

@@ -54,6 +54,8 @@ struct GemmPlan {
   int am = 128;
 };
 GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats);
+// Apply `ep` to a stream-K fp32 accumulator acc[M, N] (atomically filled) and re-zero it.
+cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& ep, cudaStream_t stream);
 
 // embed: out[r] = tok_emb[ids[r]] + pos_emb[positions[r] + pos_offset]
 cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,

@@ -120,14 +120,19 @@ def test_long_context_100k_chunk_invariance():
     one decode each.  Chunked prefill must not change the result (SURVEY §7 property): last-chunk
     and decode logits agree within the bf16 tolerance and pick the same greedy token.  Exercises
     split-KV tile attention over ~3k-page block tables and the extended position table."""
+    import os
     from paper_2503_13737_b200.executor import CudaExecutor
     from paper_2503_13737_b200.kvc import BlockPool
+    os.environ["AG_DETERMINISTIC"] = "1"  # no fp32 atomics: reproducible run to run
     P = 100_000
     cfg = M.OPTConfig("opt-13b-2l-100k", hidden=5120, num_layers=2, num_heads=40, ffn=20480,
                       max_positions=P + 64)
     w = M.init_weights(cfg, seed=3, device="cuda", init="test")
     pool = BlockPool(2 * (P // 32 + 8))
-    dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=16384, max_seqs=8, weights=w, parity_logits=True)
+    try:
+        dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=16384, max_seqs=8, weights=w, parity_logits=True)
+    finally:
+        os.environ.pop("AG_DETERMINISTIC", None)
     outs = []
     for rid, chunk in ((0, 16384), (1, 12000)):
         res = None
@@ -141,6 +146,8 @@ def test_long_context_100k_chunk_invariance():
     d_dec = (da - db).abs().max().item()
     print(f"100k prompt: max|dlogit| last-chunk {d_last:.4g}, decode {d_dec:.4g}")
     assert torch.isfinite(la).all() and torch.isfinite(da).all()
+    # the two chunkings give the GEMMs different M, hence possibly different tile / split-K plans and
+    # fp32 summation orders: equal within the bf16 tolerance (bitwise only when the plans coincide)
     assert d_last <= LOGIT_TOL and d_dec <= LOGIT_TOL
     assert ta[0] == tb[0] and tda[0] == tdb[0]
 
@@ -148,7 +155,8 @@ def test_long_context_100k_chunk_invariance():
 @pytest.mark.parametrize("splits", [2, 5, 99])  # 99 = stream-K (kStreamK)
 def test_split_k_atomic_epilogue_forward(splits):
     """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32 and the
-    next LayerNorm finishes bias + residual (and re-zeroes acc32).  Forced on for every M bucket via
+    next LayerNorm finishes bias + residual (and re-zeroes acc32); QKV / FC1 take the split-K reduce
+    kernel, or with stream-K (99) the atomic accumulator + finish kernel (q scale, KV scatter, ReLU).  Forced on for every M bucket via
     the plan table; two consecutive mixed steps vs the oracle (acc32 must be clean between steps)."""
     import ctypes as C
     from paper_2503_13737_b200.executor import CudaExecutor
@@ -160,7 +168,7 @@ def test_split_k_atomic_epilogue_forward(splits):
     rows = []
     for kind, mb, bn, ks, am in dev.gemm_plans():
         kid = ("qkv", "out", "fc1", "fc2", "lm_head").index(kind)
-        if kind in ("out", "fc2"):
+        if kind in ("out", "fc2", "qkv", "fc1"):  # QKV/FC1: reduce kernel (2, 5) / stream-K + finish (99)
             bn, ks, am = 128, splits, 128
         rows.append([kid, mb, bn, ks + 100 * am])
     buf = (C.c_int32 * (4 * len(rows)))(*[x for r in rows for x in r])

@@ -358,7 +358,9 @@ def run_reference(args):
         return
     from oracle.bench_cpu import reference_arm
     cfg, prof, prof_src, rate = build_workload(args, world)
-    res = reference_arm(cfg, prof, steps=args.steps, warmup=args.warmup)
+    # bounded CPU sample per step so the whole --steps K --warmup W run ends within a few minutes
+    tok_cap = max(16, min(256, 8192 // max(1, args.steps + args.warmup)))
+    res = reference_arm(cfg, prof, steps=args.steps, warmup=args.warmup, tok_cap=tok_cap)
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",

@@ -53,7 +53,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         s = CSRC / src
         o = obj_dir / (src + ".o")
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(s), "-o", str(o)]
+            extra = os.environ.get("NVCC_EXTRA", "").split()  # e.g. -DAG_ATTN_PIPE_PROBE for timing probes
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-c", str(s), "-o", str(o)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             r = subprocess.run(cmd, capture_output=True, text=True)

@@ -376,6 +376,15 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       const int sbuf = j & 1;
       mbar_wait(&bars->s_full[sbuf], (j >> 1) & 1);
       tc_fence_after();
+#ifdef AG_ATTN_PIPE_PROBE  // timing probe only: skip the softmax, keep the barrier protocol
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bars->s_empty[sbuf]);
+        mbar_arrive(&bars->p_full[j & 1]);
+      }
+      continue;
+#endif
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {

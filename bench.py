@@ -286,6 +286,17 @@ def run_ours(args):
                       "per_launch_bytes": attn["bytes"] / a_n if a_n else None,
                       "tflops": attn["flops"] / (attn["ms"] / 1e3) / 1e12 if attn["ms"] else 0.0},
     }
+    # traffic: DRAM bytes per launch implied by the ncu capture's DRAM / algorithmic ratio (null without it)
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        nt = json.loads(tf.read_text())
+        g_by = sum(prof_k[c]["bytes"] for c in gemm_cls)
+        for cls, per in (("attention", roof_all["attention"].get("per_launch_bytes")),
+                         ("gemm", g_by / g_n if g_n else None)):
+            if cls in nt and per:
+                ratio = nt[cls]["dram_bytes"] / nt[cls]["algorithmic_bytes"]
+                roof_all[cls]["traffic"] = per * ratio
+                roof_all[cls]["traffic_source"] = f"ncu dram/algorithmic = {ratio:.3f} ({nt[cls]['case']})"
     roof_dominant = max(roof_all.values(), key=lambda r: r["share"] or 0.0)
     line = {
         "metric": METRIC,

@@ -991,8 +991,10 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
                                   ag::GemmPlan{64, 4}, ag::GemmPlan{256, 6}, ag::GemmPlan{128, 6},
                                   ag::GemmPlan{256, 8}, ag::GemmPlan{128, 8}})
       cands.push_back({q.bn, q.k_splits, am});
-  for (int am : {128, 64, 32})  // stream-K (atomic fp32 epilogue: out-proj / FC2 at TP=1 only)
+  for (int am : {128, 64, 32})  // stream-K (atomic fp32 epilogue; finished by LayerNorm or the finish kernel)
     for (int bn : {256, 128, 64}) cands.push_back({bn, ag::kStreamK, am});
+  cands.push_back({256, ag::kStreamK, 256});  // stream-K over CTA pairs
+  cands.push_back({128, ag::kStreamK, 256});
   cudaEvent_t e0, e1;
   AG_CUDA(cudaEventCreate(&e0));
   AG_CUDA(cudaEventCreate(&e1));
@@ -1021,7 +1023,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.am < 128 && M > p.am) continue;
         if (p.k_splits == ag::kStreamK) {
-          if (p.am == 256 || k == kGemmLm) continue;
+          if (k == kGemmLm || (p.am == 256 && M < 256)) continue;
           if ((k == kGemmOut || k == kGemmFc2) && c.tp_size != 1) continue;
         } else {
           const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;

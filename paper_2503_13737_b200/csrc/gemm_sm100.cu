@@ -131,10 +131,10 @@ AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const u
 // segments; every CTA streams the same number of weight k-blocks (no wave quantisation), and
 // partial tiles meet in the atomic fp32 epilogue (kEpiAtomicF32 only).
 struct SegIter {
-  int num_m, num_kb, k_splits, kb_per, num_tiles, t;
+  int num_m, num_kb, k_splits, kb_per, num_tiles, t, stride;
   long long u, u_end;
   bool streamk;
-  AG_DEVICE SegIter(int M, int N, int K, int bm, int bn, int ks) {
+  AG_DEVICE SegIter(int M, int N, int K, int bm, int bn, int ks, int idx, int count) {
     num_m = (M + bm - 1) / bm;
     const int num_n = (N + bn - 1) / bn;
     num_kb = (K + kBK - 1) / kBK;
@@ -142,10 +142,11 @@ struct SegIter {
     k_splits = streamk ? 1 : ks;
     kb_per = (num_kb + k_splits - 1) / k_splits;
     num_tiles = num_m * num_n * k_splits;
-    t = blockIdx.x;
+    t = idx;
+    stride = count;
     const long long U = static_cast<long long>(num_m) * num_n * num_kb;
-    u = U * blockIdx.x / gridDim.x;
-    u_end = U * (blockIdx.x + 1) / gridDim.x;
+    u = U * idx / count;
+    u_end = U * (idx + 1) / count;
   }
   AG_DEVICE bool next(int& m_blk, int& n_blk, int& ks_idx, int& kb0, int& kb1) {
     if (streamk) {
@@ -165,7 +166,7 @@ struct SegIter {
     n_blk = t / (num_m * k_splits);
     kb0 = ks_idx * kb_per;
     kb1 = min(num_kb, kb0 + kb_per);
-    t += gridDim.x;
+    t += stride;
     return true;
   }
 };
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_w = num_m <= 2 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(M, N, K, kBM, BN, k_splits);
+      SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      SegIter it(M, N, K, kBM, BN, k_splits);
+      SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
-    SegIter it(M, N, K, kBM, BN, k_splits);
+    SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
     while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -352,10 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
   const int num_m = (M + 255) / 256;
-  const int num_n = (N + BN - 1) / BN;
-  const int num_kb_total = (K + kBK - 1) / kBK;
-  const int kb_per = (num_kb_total + k_splits - 1) / k_splits;
-  const int num_tiles = num_m * num_n * k_splits;
+  int m_blk, n_blk, ks, kb0, kb1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -384,12 +382,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < num_tiles; t += num_pairs) {
-        const int m_blk = t % num_m;
-        const int ks = (t / num_m) % k_splits;
-        const int n_blk = t / (num_m * k_splits);
-        const int kb0 = ks * kb_per;
-        const int kb1 = min(num_kb_total, kb0 + kb_per);
+      SegIter it(M, N, K, 256, BN, k_splits, pair, num_pairs);
+      while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
@@ -411,13 +405,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < num_tiles; t += num_pairs) {
+      SegIter it(M, N, K, 256, BN, k_splits, pair, num_pairs);
+      while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int ks = (t / num_m) % k_splits;
-        const int kb0 = ks * kb_per;
-        const int kb1 = min(num_kb_total, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -443,10 +435,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < num_tiles; t += num_pairs) {
-      const int m_blk = t % num_m;
-      const int ks = (t / num_m) % k_splits;
-      const int n_blk = t / (num_m * k_splits);
+    SegIter it(M, N, K, 256, BN, k_splits, pair, num_pairs);
+    while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row0 = m_blk * 256 + static_cast<int>(rank) * 128 + ew * 32;
@@ -617,10 +607,11 @@ static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * k_splits;
+  const int64_t tiles = static_cast<int64_t>((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int64_t units = k_splits == kStreamK ? tiles * ((K + kBK - 1) / kBK) : tiles * k_splits;
   int grid = num_sms() & ~1;
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas & ~1;
-  if (2 * units < grid) grid = 2 * units;
+  if (2 * units < grid) grid = static_cast<int>(2 * units);
   gemm2_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
@@ -635,7 +626,7 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
                         int am) {
   if (M <= 0) return cudaSuccess;
   if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
-    if (k_splits == kStreamK) return cudaErrorInvalidValue;
+    if (k_splits == kStreamK && ep.mode != kEpiAtomicF32) return cudaErrorInvalidValue;
     if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;
     if (bn == 256) return launch_bn2<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 128) return launch_bn2<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);

@@ -152,8 +152,9 @@ def test_long_context_100k_chunk_invariance():
     assert ta[0] == tb[0] and tda[0] == tdb[0]
 
 
-@pytest.mark.parametrize("splits", [2, 5, 99])  # 99 = stream-K (kStreamK)
-def test_split_k_atomic_epilogue_forward(splits):
+@pytest.mark.parametrize("bn,splits,am", [(128, 2, 128), (128, 5, 128), (128, 99, 128), (256, 99, 256),
+                                          (256, 2, 256)])  # 99 = stream-K (kStreamK); am 256 = CTA pair
+def test_split_k_atomic_epilogue_forward(bn, splits, am):
     """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32 and the
     next LayerNorm finishes bias + residual (and re-zeroes acc32); QKV / FC1 take the split-K reduce
     kernel, or with stream-K (99) the atomic accumulator + finish kernel (q scale, KV scatter, ReLU).  Forced on for every M bucket via
@@ -166,10 +167,12 @@ def test_split_k_atomic_epilogue_forward(splits):
     pool = BlockPool(1024)
     dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=1024, max_seqs=64, weights=w, parity_logits=True)
     rows = []
+    bn_, am_ = bn, am
     for kind, mb, bn, ks, am in dev.gemm_plans():
         kid = ("qkv", "out", "fc1", "fc2", "lm_head").index(kind)
         if kind in ("out", "fc2", "qkv", "fc1"):  # QKV/FC1: reduce kernel (2, 5) / stream-K + finish (99)
-            bn, ks, am = 128, splits, 128
+            bn, ks = bn_, splits
+            am = am_ if mb >= 256 or am_ != 256 else 128  # the pair kernel needs >= 256-row buckets
         rows.append([kid, mb, bn, ks + 100 * am])
     buf = (C.c_int32 * (4 * len(rows)))(*[x for r in rows for x in r])
     from paper_2503_13737_b200 import _lib
@@ -182,7 +185,7 @@ def test_split_k_atomic_epilogue_forward(splits):
         n = len(b.logit_rows)
         worst = max(worst, (a.logits[:n] - r.logits[:n]).abs().max().item())
         assert np.array_equal(a.token_ids[:n], r.token_ids[:n])
-    print(f"split-K {splits} atomic epilogue: max|dlogit|={worst:.4g}")
+    print(f"plan {bn_}x{splits}a{am_}: max|dlogit|={worst:.4g}")
     assert worst <= 5e-2
 
 

@@ -166,15 +166,21 @@ def run_ours(args):
     if rank != 0:
         # followers: mirror rank 0's steps; report own device time for the max-over-ranks
         ex.set_profiling(False)
-        dev = {"t": 0.0}
+        dev = {"t": 0.0, "on": False}  # device time of the timed steps only (leader marks 1 / 0)
         inner = ex.execute
 
         def timed_exec(b):
             r = inner(b)
-            dev["t"] += r.device_s
+            if dev["on"]:
+                dev["t"] += r.device_s
             return r
+
+        def on_mark(tag):  # timed-region bracket: device sync + barrier with rank 0
+            torch.cuda.synchronize()
+            dist.barrier()
+            dev["on"] = tag == 1
         ex.execute = timed_exec
-        TP.follower_loop(ex, group)
+        TP.follower_loop(ex, group, on_mark)
         t = torch.tensor([dev["t"]], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -211,9 +217,10 @@ def run_ours(args):
     launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
     sampler = ClockSampler(local)
     sampler.start()
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
+    if world > 1:
+        executor.mark(1)  # followers synchronise, join the barrier and start counting device time
+        dist.barrier()
     ncu_window = os.environ.get("AG_NCU_TIMED") == "1"  # ncu --profile-from-start off: timed steps only
     if ncu_window:
         torch.cuda.cudart().cudaProfilerStart()
@@ -224,6 +231,9 @@ def run_ours(args):
     if ncu_window:
         torch.cuda.cudart().cudaProfilerStop()
     clocks = sampler.stop()
+    if world > 1:
+        executor.mark(0)
+        dist.barrier()
     ex.execute = orig_exec
     dev_s = sum(r.device_s for r in recs)
     launches_timed = ex.launches - launches0

@@ -15,7 +15,7 @@ import torch.distributed as dist
 
 from .engine import DeviceBatch, StepResult
 
-OP_STOP, OP_STEP, OP_SWAP_OUT, OP_SWAP_IN = 0, 1, 2, 3
+OP_STOP, OP_STEP, OP_SWAP_OUT, OP_SWAP_IN, OP_MARK = 0, 1, 2, 3, 4
 _HDR = 8
 
 
@@ -78,11 +78,15 @@ class TPLeader:
         self._swap(OP_SWAP_IN, request_id, block_ids, tokens)
         self.local.swap_in(request_id, block_ids, tokens)
 
+    def mark(self, tag: int) -> None:
+        """Forward a marker (e.g. timed-region begin / end) to the followers' on_mark callback."""
+        _bcast_msg(torch.tensor([OP_MARK, tag, 0, 0, 0, 0, 0, 0], dtype=torch.int64), None, self.group)
+
     def stop(self) -> None:
         _bcast_msg(torch.zeros(_HDR, dtype=torch.int64), None, self.group)
 
 
-def follower_loop(local, group) -> int:
+def follower_loop(local, group, on_mark=None) -> int:
     """Ranks > 0: mirror rank 0's steps until OP_STOP; returns the number of steps executed."""
     steps = 0
     while True:
@@ -101,6 +105,8 @@ def follower_loop(local, group) -> int:
             local.swap_out(int(hdr[1]), payload.tolist(), int(hdr[2]))
         elif op == OP_SWAP_IN:
             local.swap_in(int(hdr[1]), payload.tolist(), int(hdr[2]))
+        elif op == OP_MARK and on_mark is not None:
+            on_mark(int(hdr[1]))
 
 
 def share_nccl_id(rank: int, group) -> bytes:

@@ -58,3 +58,20 @@ def test_calibrate_idempotent_and_derive(tmp_path):
     gpu.write_text(json.dumps({"peak_flops": 126.96e12}))
     assert cli.main(["calibrate", "--profile", str(part), "--gpu", str(gpu), "--out", str(out)]) == 0
     assert json.loads(out.read_text())["pivot_forward_size"] > 0
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_run_on_the_b200_executor(tmp_path):
+    """`run --executor cuda`: the engine drives the OPT-13B forward on the GPU (device clock)."""
+    tr = tmp_path / "t.jsonl"
+    assert cli.main(["gen", "--out", str(tr), "--requests", "30", "--rate", "8", "--long-fraction", "0"]) == 0
+    rc = cli.main(["run", "--trace", str(tr), "--policy", "accelgen", "--executor", "cuda", "--horizon", "2",
+                   "--profile", "profiles/opt13b_b200_tp1.json", "--out", str(tmp_path / "o")])
+    assert rc == 0
+    rows = (tmp_path / "o" / "report.csv").read_text().strip().splitlines()
+    assert len(rows) == 2 and rows[1].startswith("accelgen,")
+    rep = json.loads((tmp_path / "o" / "report_accelgen.json").read_text())
+    assert rep["tokens_per_s"] > 0

@@ -118,3 +118,63 @@ def test_pack_unpack_roundtrip():
         for f in ("token_ids", "positions", "cu_q", "ctx_len", "block_table", "slot_mapping", "logit_rows"):
             assert np.array_equal(getattr(b, f), getattr(c, f))
         assert c.request_ids == b.request_ids and c.logit_request_ids == b.logit_request_ids
+
+
+class _CountExec:
+    vocab, max_tokens, max_seqs = 50272, 1 << 20, 1 << 20
+
+    def __init__(self):
+        self.n = 0
+
+    def execute(self, b):
+        self.n += 1
+
+
+def _mark_worker(rank, world, port, q):
+    """bench.py's timed-region protocol: the leader marks begin/end and joins a barrier; followers
+    join it from the on_mark callback inside follower_loop, counting only the steps in between."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = M.OPTConfig("tp-test", hidden=256, num_layers=2, num_heads=2, ffn=1024, max_positions=256)
+    bs = _batches(cfg)
+    ex = _CountExec()
+    if rank == 0:
+        leader = tp.TPLeader(ex, dist.group.WORLD)
+        leader.execute(bs[0])          # warm-up step (not counted)
+        leader.mark(1)
+        dist.barrier()
+        leader.execute(bs[1])
+        leader.execute(bs[2])          # 2 timed steps
+        leader.mark(0)
+        dist.barrier()
+        leader.execute(bs[0])          # replay step (not counted)
+        leader.stop()
+    else:
+        state = {"on": False, "timed": 0}
+
+        class Counting(_CountExec):
+            def execute(self, b):
+                if state["on"]:
+                    state["timed"] += 1
+
+        def on_mark(tag):
+            dist.barrier()
+            state["on"] = tag == 1
+        tp.follower_loop(Counting(), dist.group.WORLD, on_mark)
+        q.put(state["timed"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_timed_region_markers_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mark_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    timed = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert timed == 2

@@ -28,7 +28,7 @@ import numpy as np
 from .cost_model import ModelProfile, iteration_time
 from .errors import AllocationError, EngineFault, StateError
 from .kvc import BlockPool
-from .policies import BatchPlan, PlanContext, PolicyConfig, Selection, has_prompt_left, plan as make_plan
+from .policies import BatchPlan, PlanContext, PolicyConfig, has_prompt_left, plan as make_plan
 from .sched_core import (ChunkStats, Phase, QueueEntry, jct_allowance, jct_initial_estimate, order_queue,
                          propagate_debt)
 from .workload import RequestSpec, SLOKind

@@ -190,32 +190,55 @@ class CudaExecutor:
         return StepResult(token_ids=out[:n].copy(), elapsed_s=dev_s, device_s=dev_s, wall_s=wall, logits=logits)
 
     # ---------------------------------------------------------------- preemption swap (kvc.py:153-160)
+    _SWAP_STAGE_BYTES = 512 << 20  # device staging for KV swaps (a request's KV can be tens of GB)
+
+    def _swap_stage(self) -> tuple[torch.Tensor, int]:
+        """Persistent device staging buffer [L, 2, chunk, heads, 32, 128] and its block capacity."""
+        per_block = self.cfg.num_layers * 2 * self.heads_l * self.block_size * HEAD_DIM * 2
+        chunk = max(1, self._SWAP_STAGE_BYTES // per_block)
+        if getattr(self, "_stage", None) is None:
+            self._stage = torch.empty(self.cfg.num_layers, 2, chunk, self.heads_l, self.block_size, HEAD_DIM,
+                                      dtype=torch.bfloat16, device=self.device)
+        return self._stage, chunk
+
     def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
+        """Preemption (reference BlockPool.preempt, kvc.py:153-160): gather the request's KV blocks
+        of every layer into the device staging buffer chunk by chunk (block_copy kernel), then copy
+        each chunk to pinned host memory."""
         if not block_ids:
             return
-        ids = torch.tensor(block_ids, dtype=torch.int32, device=self.device)
-        n = len(block_ids)
-        stage = torch.empty(self.cfg.num_layers, 2, n, self.heads_l, self.block_size, HEAD_DIM,
-                            dtype=torch.bfloat16, device=self.device)
-        for l in range(self.cfg.num_layers):
-            for kv in range(2):
-                K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv])
-        host = torch.empty(stage.shape, dtype=torch.bfloat16, pin_memory=True)
-        host.copy_(stage, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        self._swapped[request_id] = host
+        stage, chunk = self._swap_stage()
+        host_chunks = []
+        for c0 in range(0, len(block_ids), chunk):
+            ids = torch.tensor(block_ids[c0:c0 + chunk], dtype=torch.int32, device=self.device)
+            n = ids.numel()
+            for l in range(self.cfg.num_layers):
+                for kv in range(2):
+                    K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv, :n])
+            host = torch.empty((self.cfg.num_layers, 2, n) + tuple(stage.shape[3:]), dtype=torch.bfloat16,
+                               pin_memory=True)
+            host.copy_(stage[:, :, :n], non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()  # staging is reused by the next chunk
+            host_chunks.append(host)
+        self._swapped[request_id] = host_chunks
 
     def swap_in(self, request_id: int, block_ids: list[int], tokens: int) -> None:
-        host = self._swapped.pop(request_id, None)
-        if host is None:
+        host_chunks = self._swapped.pop(request_id, None)
+        if host_chunks is None:
             if tokens > 0:
                 raise EngineFault(f"request {request_id} readmitted without swapped KV")
             return
-        n = host.shape[2]
-        if len(block_ids) < n:
+        n_total = sum(h.shape[2] for h in host_chunks)
+        if len(block_ids) < n_total:
             raise EngineFault("readmission allocated fewer blocks than were swapped out")
-        ids = torch.tensor(block_ids[:n], dtype=torch.int32, device=self.device)
-        stage = host.to(self.device, non_blocking=True)
-        for l in range(self.cfg.num_layers):
-            for kv in range(2):
-                K.kv_swap_in(stage[l, kv], ids, self.kv[l, kv])
+        stage, _ = self._swap_stage()
+        at = 0
+        for host in host_chunks:
+            n = host.shape[2]
+            ids = torch.tensor(block_ids[at:at + n], dtype=torch.int32, device=self.device)
+            stage[:, :, :n].copy_(host, non_blocking=True)
+            for l in range(self.cfg.num_layers):
+                for kv in range(2):
+                    K.kv_swap_in(stage[l, kv, :n], ids, self.kv[l, kv])
+            torch.cuda.current_stream(self.device).synchronize()  # staging is reused by the next chunk
+            at += n

@@ -218,3 +218,24 @@ def test_175b_shape_two_layers_vs_oracle():
     # and require the greedy token wherever the oracle's top-2 gap exceeds that bound
     assert worst <= 1e-2 * scale
     assert agree >= total - sum(g <= 2 * worst for g in gaps)
+
+
+def test_executor_swap_roundtrip_chunked():
+    """Preemption swap through the executor (kvc.py:153-160 preempt / demand_readmit): a request's
+    blocks of every layer go to host memory through a bounded device staging buffer in several
+    chunks, and come back bit-exactly into different physical blocks."""
+    from paper_2503_13737_b200.executor import CudaExecutor
+    cfg = M.tiny()
+    w = M.init_weights(cfg, seed=0, init="test")
+    dev = CudaExecutor(cfg, 64, max_tokens=256, max_seqs=8, weights=w, autotune=False)
+    dev._SWAP_STAGE_BYTES = 3 * cfg.num_layers * 2 * dev.heads_l * 32 * 128 * 2  # 3 blocks per chunk
+    g = torch.Generator(device="cuda").manual_seed(3)
+    dev.kv.copy_(torch.randn(dev.kv.shape, generator=g, device="cuda").to(torch.bfloat16))
+    src = [5, 9, 2, 40, 41, 17, 63, 0]
+    before = dev.kv[:, :, src].clone()
+    dev.swap_out(7, src, 8 * 32)
+    assert len(dev._swapped[7]) == 3                 # ceil(8 / 3) chunks
+    dev.kv[:, :, src] = 0
+    dst = [10, 11, 12, 13, 14, 15, 16, 18]
+    dev.swap_in(7, dst, 8 * 32)
+    assert torch.equal(dev.kv[:, :, dst], before)

@@ -201,6 +201,15 @@ class CudaExecutor:
                                       dtype=torch.bfloat16, device=self.device)
         return self._stage, chunk
 
+    def _host_buffer(self, shape) -> torch.Tensor:
+        """Pinned host memory for swapped KV; pageable when the OS refuses to lock more pages."""
+        if not getattr(self, "_pin_failed", False):
+            try:
+                return torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+            except (RuntimeError, torch.AcceleratorError):
+                self._pin_failed = True
+        return torch.empty(shape, dtype=torch.bfloat16)
+
     def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
         """Preemption (reference BlockPool.preempt, kvc.py:153-160): gather the request's KV blocks
         of every layer into the device staging buffer chunk by chunk (block_copy kernel), then copy
@@ -215,9 +224,8 @@ class CudaExecutor:
             for l in range(self.cfg.num_layers):
                 for kv in range(2):
                     K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv, :n])
-            host = torch.empty((self.cfg.num_layers, 2, n) + tuple(stage.shape[3:]), dtype=torch.bfloat16,
-                               pin_memory=True)
-            host.copy_(stage[:, :, :n], non_blocking=True)
+            host = self._host_buffer((self.cfg.num_layers, 2, n) + tuple(stage.shape[3:]))
+            host.copy_(stage[:, :, :n], non_blocking=host.is_pinned())
             torch.cuda.current_stream(self.device).synchronize()  # staging is reused by the next chunk
             host_chunks.append(host)
         self._swapped[request_id] = host_chunks
@@ -236,7 +244,7 @@ class CudaExecutor:
         for host in host_chunks:
             n = host.shape[2]
             ids = torch.tensor(block_ids[at:at + n], dtype=torch.int32, device=self.device)
-            stage[:, :, :n].copy_(host, non_blocking=True)
+            stage[:, :, :n].copy_(host, non_blocking=host.is_pinned())
             for l in range(self.cfg.num_layers):
                 for kv in range(2):
                     K.kv_swap_in(stage[l, kv, :n], ids, self.kv[l, kv])

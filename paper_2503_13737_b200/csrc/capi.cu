@@ -954,7 +954,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   const int H = c.hidden;
   GemmTable& t = m->tune;
   t.m_bucket.clear();
-  for (int mb : {16, 32, 64, 128, 192, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288, 16384})
+  for (int mb : {16, 32, 64, 128, 192, 256, 320, 384, 448, 512, 640, 768, 896, 1024, 1280, 1536, 2048, 3072, 4096,
+                 6144, 8192, 12288, 16384})
     if (mb < c.max_tokens) t.m_bucket.push_back(mb);
   t.m_bucket.push_back(c.max_tokens);
   const size_t T = align_up(static_cast<size_t>(c.max_tokens), 128);

@@ -40,6 +40,7 @@ def cmd_gen(args) -> int:
     """JSONL trace + printed summary."""
     prof = cm.load_profile(args.profile) if args.profile else cm.opt_13b_like()
     cfg = workload.TraceConfig(num_requests=args.requests, arrival_rate=args.rate, long_fraction=args.long_fraction,
+                               long_len_dist=workload.LengthDist(kind="log_uniform", lo=args.long_lo, hi=args.long_hi),
                                offline_fraction=args.offline_fraction, seed=args.seed, profile=prof)
     trace = workload.generate_trace(cfg)
     workload.save_trace(trace, args.out)
@@ -151,6 +152,8 @@ def build_parser() -> argparse.ArgumentParser:
     g.add_argument("--rate", type=float, default=8.0)
     g.add_argument("--long-fraction", type=float, default=0.35)
     g.add_argument("--offline-fraction", type=float, default=0.0)
+    g.add_argument("--long-lo", type=int, default=4096)
+    g.add_argument("--long-hi", type=int, default=100000)
     g.add_argument("--seed", type=int, default=0)
     g.add_argument("--profile", default=None)
     r = sub.add_parser("run")

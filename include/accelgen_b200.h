@@ -3,7 +3,7 @@
  *
  * This library replaces ONE call in the reference: the simulated GPU step.  In the reference,
  * engine.step "advance[s] clock by iteration_time(S_f)" where iteration_time is
- * the linear stand-in  T_0 + T_pf * S_f / S_pf  (pkg/src/slosim/cost_model.py:133-141).  Here the
+ * the linear stand-in  T_0 + T_pf * S_f / S_pf  (pkg/src/slosim/cost_model.py:101-109).  Here the
  * BatchPlan that AccelGen's policy packs is executed on the GPU instead:
  * embedding -> L x [LN, QKV(+paged KV append), mixed paged attention, out-proj(+TP all-reduce),
  * LN, FC1+ReLU, FC2(+TP all-reduce)] -> final LN on the logit rows -> LM head -> argmax.
@@ -58,7 +58,7 @@ enum {
 };
 
 /* Model shape and capacities.  Mirrors the reference ModelProfile's shape fields
- * (cost_model.py:66-76: hidden_size, num_layers, bytes_per_element) plus the OPT architecture
+ * (cost_model.py:34-58: hidden_size, num_layers, bytes_per_element) plus the OPT architecture
  * constants the cost model folds away. */
 typedef struct {
   int32_t hidden;          /* H (5120 for OPT-13B) */

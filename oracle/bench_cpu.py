@@ -1,6 +1,6 @@
 """CPU timing of the oracle forward — TEST/BASELINE INFRASTRUCTURE ONLY (bench.py's cpu_baseline
 and --impl reference legs).  The reference has no forward of its own (its GPU is the linear
-iteration_time model, cost_model.py:133-141), so the "reference CPU path" is this repo's CPU
+iteration_time model, cost_model.py:101-109), so the "reference CPU path" is this repo's CPU
 restatement: oracle.sched (policies + engine) producing the BatchPlans and oracle.forward
 executing them, with all host threads.
 """

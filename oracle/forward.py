@@ -5,7 +5,7 @@ import this module.  The product path (paper_2503_13737_b200) never does.
 
 What it restates
   The reference ships no forward pass: its "GPU" is the linear stand-in iteration_time
-  (pkg/src/slosim/cost_model.py:133-141) and the paper's executor was vLLM + FlashAttention-2
+  (pkg/src/slosim/cost_model.py:101-109) and the paper's executor was vLLM + FlashAttention-2
   (PAPER.md:2002-2009), neither of which is under /root/reference.  Logit parity is therefore
   "parity unpinned" by the reference itself.  This oracle restates the OPT decoder the paper
   serves (per-layer QKV, attention, out-proj, FC1, FC2, residuals; the operation

@@ -4,7 +4,7 @@ Architecture (pre-LN OPT, as in transformers ``modeling_opt.py`` OPTDecoderLayer
 positions with offset 2, q scaled by head_dim^-0.5, LayerNorm before attention and before the
 MLP, ReLU FC1, biases everywhere, final LayerNorm, LM head tied to the token embedding.  The
 paper serves OPT-13B and OPT-175B; the reference folds the model into
-``hidden_size``/``num_layers`` of ModelProfile (pkg/src/slosim/cost_model.py:66-76).
+``hidden_size``/``num_layers`` of ModelProfile (pkg/src/slosim/cost_model.py:34-58).
 
 Weights are generated per (layer, tensor) from a keyed seed so every rank can materialise
 exactly its own shard of the same global model (no checkpoint exists offline).
@@ -49,7 +49,7 @@ class OPTConfig:
         return L * per_layer + self.vocab * H + self.pos_rows * H + 2 * H
 
     def kv_bytes_per_token(self, tp: int = 1, bytes_per_element: int = 2) -> int:
-        """2 * bytes * L * H / tp  (reference kvc_bytes_per_token, cost_model.py:128-130)."""
+        """2 * bytes * L * H / tp  (reference kvc_bytes_per_token, cost_model.py:96-98)."""
         return 2 * bytes_per_element * self.num_layers * self.hidden // tp
 
 

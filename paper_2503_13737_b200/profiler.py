@@ -4,7 +4,7 @@ The paper finds the pivot forward size S_pf by sweeping the forward size until t
 saturates and records the batch time T_pf there (PAPER §4.2, "we measure the pivot forward size
 (S_pf) by varying the forward size ... and measure the corresponding batch execution time";
 the saturation criterion <3% marginal gain is in PAPER.md:726).  The reference's stand-in only
-derives it from a peak FLOP/s (cost_model.py:144-159).  Here the sweep runs the real mixed
+derives it from a peak FLOP/s (cost_model.py:112-127).  Here the sweep runs the real mixed
 forward on the GPU (CUDA-event time of ag_model_forward), fits the reference's linear model
 T(S_f) = T_0 + T_pf * S_f / S_pf by least squares, and writes a ModelProfile JSON
 (PROFILE_KEYS, cost_model.py:23-31) that bench.py / the engine load with load_profile.

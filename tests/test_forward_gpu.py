@@ -239,3 +239,34 @@ def test_executor_swap_roundtrip_chunked():
     dst = [10, 11, 12, 13, 14, 15, 16, 18]
     dev.swap_in(7, dst, 8 * 32)
     assert torch.equal(dev.kv[:, :, dst], before)
+
+
+def test_forward_at_capacity_limits():
+    """S_f exactly max_tokens, a sequence filling its block-table row, logit rows for every sequence,
+    and the C ABI's capacity checks (EngineFault / AllocationError instead of a bad launch)."""
+    from paper_2503_13737_b200.errors import AllocationError, EngineFault
+    from paper_2503_13737_b200.executor import CudaExecutor
+    from paper_2503_13737_b200.kvc import BlockPool
+    cfg = M.tiny()
+    w = M.init_weights(cfg, seed=2, init="test")
+    pool = BlockPool(256)
+    dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=384, max_seqs=4, max_blocks_per_seq=16, weights=w,
+                       parity_logits=True)
+    ref = OracleExecutor(cfg, w, pool.total_blocks)
+    b = _make_batch(pool, cfg, [(0, 0, 200), (1, 0, 184)])   # S_f = 384 = max_tokens
+    a, r = dev.execute(b), ref.execute(b)
+    assert (a.logits[:2] - r.logits[:2]).abs().max().item() <= LOGIT_TOL
+    b = _make_batch(pool, cfg, [(2, 0, 385)])                  # 385 > max_tokens
+    with pytest.raises((AllocationError, EngineFault)):
+        dev.execute(b)
+    b = _make_batch(pool, cfg, [(3, 0, 300)])
+    dev.execute(b)
+    b = _make_batch(pool, cfg, [(3, 300, 300)])                # 600 tokens = 19 blocks > max_blocks_per_seq
+    with pytest.raises((AllocationError, EngineFault)):
+        dev.execute(b)
+    pool2 = BlockPool(256)
+    b = _make_batch(pool2, cfg, [(5, 0, 300), (6, 0, 10)])
+    a, r = dev.execute(b), ref.execute(b)
+    b = _make_batch(pool2, cfg, [(5, 300, 212)])               # ctx 300 + 212 = 512 tokens = 16 blocks
+    a, r = dev.execute(b), ref.execute(b)
+    assert (a.logits[:1] - r.logits[:1]).abs().max().item() <= LOGIT_TOL

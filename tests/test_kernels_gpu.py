@@ -197,6 +197,26 @@ def test_mixed_attention(K, seqs, heads):
     assert err <= 2e-2, err
 
 
+@pytest.mark.parametrize("seqs,heads", [
+    # row path (q <= 16) vs tile path (q >= 17) boundary, at page (32) / KV-tile (128) boundaries
+    ([(0, 16), (0, 17), (31, 16), (32, 17), (127, 1), (128, 1), (129, 17)], 3),
+    ([(96, 31), (128, 128), (255, 129), (0, 257)], 2),
+    # decode rows whose context straddles the split sizes (64-aligned row splits)
+    ([(511, 1), (512, 1), (1023, 1), (1024, 1), (4095, 1), (4097, 1)], 4),
+    # one long causal chunk over many tiles, heads of the 13B shard count
+    ([(0, 1000)], 40),
+    # chunk whose causal end is inside the first KV tile of a split
+    ([(12000, 130), (7, 3)], 2),
+])
+def test_mixed_attention_boundaries(K, seqs, heads):
+    q, kp, vp, bt, cu, ctx = _attn_case(seqs, heads, seed=sum(c + n for c, n in seqs) % 997)
+    out = K.paged_attention(q.to(DEV), kp.to(DEV), vp.to(DEV), bt.to(DEV), cu, ctx)
+    torch.cuda.synchronize()
+    ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
+    err = (out.float().cpu() - ref).abs().max().item()
+    assert err <= 2e-2, err
+
+
 def test_kv_swap_roundtrip(K):
     pool = _bf((50, 2, 32, 128), 16).to(DEV)
     ids = torch.tensor([4, 9, 0, 31], dtype=torch.int32, device=DEV)

@@ -109,6 +109,12 @@ def default_profile(tp: int):
     p = ROOT / "profiles" / f"opt13b_b200_tp{tp}.json"
     if p.exists():
         return cm.load_profile(p), str(p.relative_to(ROOT))
+    p1 = ROOT / "profiles" / "opt13b_b200_tp1.json"
+    if p1.exists():  # no TP-t measurement yet: the TP=1 measurement with the linear work split by t
+        base = cm.load_profile(p1)
+        return cm.ModelProfile(**{**base.__dict__, "pivot_time_s": base.pivot_time_s / tp,
+                                  "fixed_overhead_s": base.fixed_overhead_s / tp}), \
+            f"{p1.relative_to(ROOT)} scaled 1/{tp} (TP={tp} not measured yet)"
     # declared fallback until the profiler has written one: S_pf 2048, linear fit guess
     return cm.ModelProfile(hidden_size=5120, num_layers=40, pivot_forward_size=2048, pivot_time_s=0.06 / tp,
                            fixed_overhead_s=0.006 / tp, kvc_capacity_tokens=0), "declared-default"
@@ -154,6 +160,10 @@ def run_ours(args):
         free_b = torch.cuda.mem_get_info()[0]
         args.kv_gb = max(1.0, (free_b - 2.0 * mcfg.param_count() / world - 12e9) / 1e9)
     num_blocks = int(args.kv_gb * 1e9 // (32 * kv_tok_bytes))
+    if world > 1:  # one pool geometry for all ranks: rank 0's block ids index every rank's pool
+        nb = torch.tensor([num_blocks], dtype=torch.int64)
+        dist.all_reduce(nb, op=dist.ReduceOp.MIN)
+        num_blocks = int(nb.item())
     prof = ModelProfile(**{**prof.__dict__, "kvc_capacity_tokens": num_blocks * 32})
     uid = TP.share_nccl_id(rank, group) if world > 1 else None
     s_pf = prof.pivot_forward_size

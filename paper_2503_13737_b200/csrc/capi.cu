@@ -162,9 +162,11 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
 // ---------------------------------------------------------------- model object
 // A weight operand needs one tensor map per N-tile width (the TMA box must equal BLOCK_N).
 struct WeightMap {
-  CUtensorMap box64, box128, box256;
-  bool has256 = false;
-  const CUtensorMap& box(int bn) const { return bn == 256 ? box256 : (bn == 64 ? box64 : box128); }
+  CUtensorMap box64, box128, box160, box256;
+  bool has256 = false, has160 = false;
+  const CUtensorMap& box(int bn) const {
+    return bn == 256 ? box256 : (bn == 160 ? box160 : (bn == 64 ? box64 : box128));
+  }
 };
 
 // Activation operand maps for the three A-box heights (128 rows; 32/64 for small-M GEMMs).
@@ -276,6 +278,8 @@ int32_t wmap(WeightMap* w, const void* ptr, int64_t rows, int64_t k, const char*
   AG_TRY(tmap(&w->box128, ptr, rows, k, 128, what));
   w->has256 = rows % 256 == 0;
   if (w->has256) AG_TRY(tmap(&w->box256, ptr, rows, k, 256, what));
+  w->has160 = rows % 160 == 0;  // 160-wide tiles: FC1 (20480/160 = 128 tiles) fills the SMs at small M
+  if (w->has160) AG_TRY(tmap(&w->box160, ptr, rows, k, 160, what));
   return AG_OK;
 }
 
@@ -295,6 +299,7 @@ ag::GemmPlan pick_plan(const WeightMap& w, int M, int N, int K, int64_t splitk_c
   }
   if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_cap);
   if (p.bn == 256 && !w.has256 && p.am != 256) p.bn = 128;
+  if (p.bn == 160 && (!w.has160 || p.am == 256)) p.bn = 128;
   return p;
 }
 
@@ -307,18 +312,8 @@ cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, con
     if (p.am == 256) return ag::launch_gemm(a.box(128), w.box(p.bn / 2), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, 256);
     return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
   }
-  if (tune && tune->ready && kind >= 0) {
-    for (size_t i = 0; i < tune->m_bucket.size(); ++i) {
-      if (M <= tune->m_bucket[i] || i + 1 == tune->m_bucket.size()) {
-        p = tune->plan[kind][i];
-        break;
-      }
-    }
-    if (static_cast<int64_t>(p.k_splits) * M * N > splitk_cap) p.k_splits = 1;
-    if (p.am < 128 && M > p.am) p.am = 128;
-  }
-  if (p.bn == 0) p = ag::plan_gemm(M, N, K, splitk_ws ? splitk_cap : 0);
-  if (p.bn == 256 && !w.has256 && p.am != 256) p.bn = 128;
+  p = pick_plan(w, M, N, K, splitk_ws ? splitk_cap : 0, tune, kind);
+  if (p.k_splits == ag::kStreamK && ep.mode != ag::kEpiAtomicF32) p.k_splits = 1;  // needs a deferred epilogue
   if (p.am == 256) return ag::launch_gemm(a.box(128), w.box(p.bn / 2), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, 256);
   return ag::launch_gemm(a.box(p.am), w.box(p.bn), M, N, K, p.bn, ep, 0, s, p.k_splits, splitk_ws, p.am);
 }
@@ -994,6 +989,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
       cands.push_back({q.bn, q.k_splits, am});
   for (int am : {128, 64, 32})  // stream-K (atomic fp32 epilogue; finished by LayerNorm or the finish kernel)
     for (int bn : {256, 128, 64}) cands.push_back({bn, ag::kStreamK, am});
+  for (int am : {128, 64, 32})
+    for (int ks : {1, 2}) cands.push_back({160, ks, am});
   cands.push_back({256, ag::kStreamK, 256});  // stream-K over CTA pairs
   cands.push_back({128, ag::kStreamK, 256});
   cudaEvent_t e0, e1;
@@ -1022,6 +1019,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         const ag::GemmEpilogue& eg = finish ? ea : ep;
         if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
+        if (p.bn == 160 && (!sh.w[0]->has160 || p.am == 256)) continue;
         if (p.am < 128 && M > p.am) continue;
         if (p.k_splits == ag::kStreamK) {
           if (k == kGemmLm || (p.am == 256 && M < 256)) continue;
@@ -1087,7 +1085,7 @@ int32_t ag_model_set_gemm_plans(ag_model* m, const int32_t* rows, int32_t n) {
   for (int i = 0; i < n; ++i) {
     const int kind = rows[4 * i], mb = rows[4 * i + 1], bn = rows[4 * i + 2], ks = rows[4 * i + 3] % 100,
               am = rows[4 * i + 3] / 100;
-    if (kind < 0 || kind >= kGemmKinds || mb <= 0 || (bn != 64 && bn != 128 && bn != 256) || ks < 1 ||
+    if (kind < 0 || kind >= kGemmKinds || mb <= 0 || (bn != 64 && bn != 128 && bn != 160 && bn != 256) || ks < 1 ||
         (am != 32 && am != 64 && am != 128 && am != 256))
       return fail(AG_EINVAL, "bad gemm plan row " + std::to_string(i));
     if (kind == 0) t.m_bucket.push_back(mb);
@@ -1146,7 +1144,8 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
     const int nkb = (K + 63) / 64, per = (nkb + k_splits - 1) / k_splits;
     if ((nkb + per - 1) / per != k_splits) return fail(AG_EINVAL, "k_splits leaves an empty K range");
   }
-  if (block_n != 64 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "block_n must be 64, 128 or 256");
+  if (block_n != 64 && block_n != 128 && block_n != 160 && block_n != 256)
+    return fail(AG_EINVAL, "block_n must be 64, 128, 160 or 256");
   CUtensorMap ta, tb;
   int r = ag::make_tmap_kmajor(&ta, A, std::max<int64_t>(M, 1), K, lda, a_rows == 256 ? 128 : a_rows);
   if (r) return fail(AG_EINVAL, "tensor map A failed (alignment?)");

@@ -32,7 +32,8 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagesFit = (200 * 1024) / kStageBytes;
   static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  // double-buffered accumulator; tcgen05.alloc takes a power of two >= 32 columns (BN=160 -> 512)
+  static constexpr int kTmemCols = 2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256;
 };
 
@@ -636,15 +637,18 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
   if (am != 128 && M > am) return cudaErrorInvalidValue;  // small-M variant needs one m-block
   if (am == 32) {
     if (bn == 256) return launch_bn<256, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    if (bn == 160) return launch_bn<160, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 64) return launch_bn<64, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     return launch_bn<128, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   }
   if (am == 64) {
     if (bn == 256) return launch_bn<256, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+    if (bn == 160) return launch_bn<160, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 64) return launch_bn<64, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     return launch_bn<128, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   }
   if (bn == 256) return launch_bn<256>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+  if (bn == 160) return launch_bn<160>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   if (bn == 64) return launch_bn<64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
 }

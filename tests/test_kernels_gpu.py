@@ -26,7 +26,7 @@ def _bf(shape, seed, std=1.0):
 @pytest.mark.parametrize("M,N,K_,bn", [
     (1, 256, 256, 0), (7, 768, 256, 0), (128, 256, 512, 256), (200, 1920, 640, 128), (777, 5120, 1024, 0),
     (1024, 3072, 5120, 256), (333, 50272, 256, 0), (2048, 2560, 5120, 0), (64, 1024, 4096, 128),
-    (200, 1920, 640, 64), (5, 5120, 20480, 64),
+    (200, 1920, 640, 64), (5, 5120, 20480, 64), (64, 20480, 5120, 160), (300, 1600, 1024, 160),
 ])
 @pytest.mark.parametrize("splits", [1, 3])
 def test_gemm_matches_fp32(K, M, N, K_, bn, splits):
@@ -43,6 +43,7 @@ def test_gemm_matches_fp32(K, M, N, K_, bn, splits):
 
 
 @pytest.mark.parametrize("M,N,K_,bn,splits,a_rows", [(1, 5120, 5120, 128, 1, 32), (32, 15360, 5120, 256, 2, 32),
+                                                     (40, 20480, 5120, 160, 1, 64), (17, 3200, 2048, 160, 2, 32),
                                                      (60, 2048, 20480, 64, 4, 64), (64, 20480, 5120, 256, 1, 64)])
 def test_gemm_small_m_variant(K, M, N, K_, bn, splits, a_rows):
     """Small-M path: only `a_rows` activation rows are staged; stale rows feed masked outputs only."""

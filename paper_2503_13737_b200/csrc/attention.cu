@@ -268,7 +268,33 @@ struct TileBars {
   uint32_t tmem_base;
 };
 
+#ifdef AG_ATTN_SPIN_WAIT
+#define AG_TILE_WAIT mbar_wait_spin
+#else
+#define AG_TILE_WAIT mbar_wait
+#endif
+
+#ifdef AG_ATTN_TIMELINE  // timing probe only: per-CTA globaltimer stamps (entry, setup, loop end, exit)
+__device__ unsigned long long g_attn_tl[16384 * 6];
+AG_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define AG_TL(slot, v) g_attn_tl[blockIdx.x * 6 + (slot)] = (v)
+#else
+#define AG_TL(slot, v)
+#endif
+
 AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem& it, int head, uint8_t* smem) {
+#ifdef AG_ATTN_TIMELINE
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    AG_TL(0, gtimer());
+    AG_TL(5, smid);
+  }
+#endif
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   TileBars* bars = reinterpret_cast<TileBars*>(smem + kBarOff);
@@ -298,6 +324,11 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#ifdef AG_ATTN_TIMELINE
+  if (threadIdx.x == 0) AG_TL(1, gtimer());
+#endif
+  pdl_trigger();  // only after the TMEM allocation (see gemm_bf16_tn_kernel)
+  pdl_wait();     // Q, the paged K/V and the outputs belong to the predecessor kernels
   const uint32_t tmem = bars->tmem_base;  // S0 [0,128) S1 [128,256) O [256,384)
 
   if (warp == 0) {
@@ -313,6 +344,10 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % kKVStages;
         mbar_wait(&bars->kv_empty[st], ((j / kKVStages) & 1) ^ 1);
+#ifdef AG_ATTN_PROBE_NOTMA  // timing probe only: K/V stages are not loaded (MMAs read stale smem)
+        mbar_arrive(&bars->kv_full[st]);
+        continue;
+#endif
         mbar_arrive_expect_tx(&bars->kv_full[st], kStageBytes);
         uint8_t* kdst = smem + kKVOff + st * kStageBytes;
         uint8_t* vdst = kdst + 2 * kSub;
@@ -338,28 +373,32 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
         mbar_wait(&bars->s_empty[sbuf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t kaddr = sb + kKVOff + st * kStageBytes;
+#ifndef AG_ATTN_PROBE_NOS  // timing probe only: skip the S MMAs
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint64_t a = umma_desc_sw128(sb + kQOff + (k >> 2) * kSub) + 2 * (k & 3);
           const uint64_t b = umma_desc_sw128(kaddr + (k >> 2) * kSub) + 2 * (k & 3);
           umma_bf16_ss(tmem + sbuf * 128, a, b, idesc_s, k > 0 ? 1u : 0u);
         }
+#endif
         umma_commit(&bars->s_full[sbuf]);
       };
       issue_s(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_s(j + 1);
         const int pb = j & 1, st = j % kKVStages;
-        mbar_wait(&bars->p_full[pb], (j >> 1) & 1);
+        AG_TILE_WAIT(&bars->p_full[pb], (j >> 1) & 1);
         tc_fence_after();
         // O += P_j . V_j with P_j (bf16, packed in columns 0-63 of S buffer pb) as the TMEM A operand
         const uint32_t ptmem = tmem + pb * 128;
         const uint32_t vaddr = sb + kKVOff + st * kStageBytes + 2 * kSub;
+#ifndef AG_ATTN_PROBE_NOPV  // timing probe only: skip the P.V MMAs
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA = 8 TMEM columns of packed bf16 pairs
           const uint64_t b = umma_desc_sw128_mn(vaddr + k * 2048, kSub);
           umma_bf16_ts(tmem + 256, ptmem + 8 * k, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
+#endif
         umma_commit(&bars->o_done[pb]);
         umma_commit(&bars->kv_empty[st]);
       }
@@ -374,7 +413,7 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       const int sbuf = j & 1;
-      mbar_wait(&bars->s_full[sbuf], (j >> 1) & 1);
+      AG_TILE_WAIT(&bars->s_full[sbuf], (j >> 1) & 1);
       tc_fence_after();
 #ifdef AG_ATTN_PIPE_PROBE  // timing probe only: skip the softmax, keep the barrier protocol
       tc_fence_before();
@@ -457,6 +496,12 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->p_full[j & 1]);
     }
+#ifdef AG_ATTN_TIMELINE
+    if (threadIdx.x == 64) {
+      AG_TL(2, gtimer());
+      AG_TL(4, n_tiles);
+    }
+#endif
     // epilogue: O row / l
     if (n_tiles > 0) {
       mbar_wait(&bars->o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
@@ -500,6 +545,9 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
   }
   tc_fence_before();
   __syncthreads();
+#ifdef AG_ATTN_TIMELINE
+  if (threadIdx.x == 0) AG_TL(3, gtimer());
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -518,6 +566,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tile_tc(p, tm, it, blockIdx.x / n_tile_items, smem);
     return;
   }
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5;
   const int u = (blockIdx.x - n_tile_ctas) * (kThreads / 32) + warp;
   if (u >= n_row_items * p.heads) return;
@@ -530,6 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // One warp per (query row, head), four head dims per lane; splits of a row sit `q_rows` apart.
 __global__ void __launch_bounds__(256) attn_combine_kernel(AttnParams p, const AttnCombine* __restrict__ combines,
                                                            int n_combines) {
+  pdl_trigger();
+  pdl_wait();
   const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (unit >= n_combines * p.heads) return;
   const int lane = threadIdx.x & 31;
@@ -560,6 +612,12 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(AttnParams p, const A
 
 }  // namespace
 
+#ifdef AG_ATTN_TIMELINE
+extern "C" __attribute__((visibility("default"))) int ag_debug_attn_timeline(void* dst, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(dst, g_attn_tl, sizeof(unsigned long long) * 6 * n));
+}
+#endif
+
 int attention_tile_rows() { return kTM; }
 int attention_tile_kv() { return kTN; }
 
@@ -575,13 +633,13 @@ cudaError_t launch_attention(const AttnParams& p, const AttnTmaps& tm, const Att
       attr = true;
     }
     const int ctas = n_tile_items * p.heads + (n_row_items * p.heads + kThreads / 32 - 1) / (kThreads / 32);
-    mixed_attention_kernel<<<ctas, kThreads, kSmemBytes, stream>>>(p, tm, items, n_tile_items, n_row_items);
+    (void)launch_k(kPdlAttn, mixed_attention_kernel, ctas, kThreads, kSmemBytes, stream, p, tm, items, n_tile_items, n_row_items);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (n_combines > 0) {
     const int units = n_combines * p.heads;
-    attn_combine_kernel<<<(units + 7) / 8, 256, 0, stream>>>(p, combines, n_combines);
+    (void)launch_k(kPdlAttn, attn_combine_kernel, (units + 7) / 8, 256, 0, stream, p, combines, n_combines);
     return cudaGetLastError();
   }
   return cudaSuccess;

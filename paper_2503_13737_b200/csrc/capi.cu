@@ -1052,6 +1052,9 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
           t.plan[k][b] = p;
         }
       }
+      if (std::getenv("AG_AUTOTUNE_LOG"))
+        std::fprintf(stderr, "{\"autotune\": %d, \"M\": %d, \"N\": %d, \"K\": %d, \"us\": %.2f, \"bn\": %d, \"ks\": %d, \"am\": %d}\n",
+                     k, M, sh.N, sh.K, best * 1e3f / 8, t.plan[k][b].bn, t.plan[k][b].k_splits, t.plan[k][b].am);
     }
   }
   cudaEventDestroy(e0);

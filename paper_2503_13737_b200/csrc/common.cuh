@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <utility>
+
 #define AG_DEVICE __device__ __forceinline__
 
 namespace ag {
@@ -55,9 +59,38 @@ AG_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 AG_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+#ifdef AG_DEBUG_MBAR  // debugging: report the stuck barrier quickly
+    if (++spins > (1u << 20)) {
+      printf("mbar timeout block %d/%d thread %d/%d bar 0x%x parity %u\n", (int)blockIdx.x, (int)gridDim.x,
+             (int)threadIdx.x, (int)blockDim.x, smem_u32(bar), parity);
+      __trap();
+    }
+#else
     if (++spins > (1u << 26)) {
       __trap();
     }
+#endif
+  }
+}
+
+// Poll with test_wait (never suspends): for latency-critical handoffs between one producer thread
+// and a few consumers where the try_wait suspend/wake round trip shows up on the critical path.
+AG_DEVICE bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+AG_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_test_wait(bar, parity)) {
+    if (++spins > (1u << 30)) __trap();
   }
 }
 
@@ -232,6 +265,49 @@ AG_DEVICE void tmem_alloc_cg2(uint32_t* dst_smem, uint32_t ncols) {
 
 AG_DEVICE void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The kernels of the forward chain are launched with programmatic stream serialization (launch_k):
+// a kernel's CTAs may become resident, initialise barriers / TMEM and prefetch weights while its
+// predecessor drains.  Every thread that touches memory the predecessor writes (or reads, for
+// outputs written in place) first executes griddepcontrol.wait, which returns once the
+// predecessor grid has completed and its writes are visible; every kernel executes it in at least
+// one thread of every CTA before exiting, so completion stays transitive along the chain.  Without
+// the launch attribute (AG_PDL=0, or a standalone launch) the wait returns immediately.
+AG_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+AG_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// AG_PDL=0 disables it; AG_PDL_MASK=<bits> enables it per launch class (1 GEMM, 2 attention,
+// 4 norms, 8 other) for bisection.
+enum PdlClass { kPdlGemm = 1, kPdlAttn = 2, kPdlNorm = 4, kPdlOther = 8 };
+inline bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    const char* e = std::getenv("AG_PDL");
+    if (e && e[0] == '0') return 0;
+    const char* m = std::getenv("AG_PDL_MASK");
+    // Norm kernels are not launched early (they still trigger their dependents): with GEMM -> norm
+    // -> GEMM all early-launched, the 13B mixed-batch forward hung on B200 (no mbarrier timeout:
+    // a hardware wait never returned).  GEMM, attention and the small kernels are.
+    return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlOther);
+  }();
+  return (mask & cls) != 0;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------- misc

@@ -27,6 +27,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
                              const __nv_bfloat16* __restrict__ tok_emb,
                              const __nv_bfloat16* __restrict__ pos_emb, int pos_offset, int rows,
                              int hidden, int vocab, int max_pos_rows, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int vec_per_row = hidden / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(kLNThreads)
                      const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
                      const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
                      float eps, int hidden, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[kLNThreads / 32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -154,6 +158,8 @@ __global__ void __launch_bounds__(1024)
                          const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
                          float eps, int hidden, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -225,6 +231,8 @@ __global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
     rmsnorm_warp_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                         const __nv_bfloat16* __restrict__ gamma, float eps, int rows, int hidden,
                         __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * kLNWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= rows) return;
   const int lane = threadIdx.x & 31;
@@ -273,6 +281,8 @@ __global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
 // One thread per (row, head, pair of 2 x 4 dims): 8-B vector loads/stores of both halves.
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ x, int ld, const int32_t* __restrict__ positions, int rows,
                             int heads, int head_dim, int rotary_dim, float log2_theta) {
+  pdl_trigger();
+  pdl_wait();
   const int half = rotary_dim / 2;
   const int quads = half / 4;
   const int64_t total = static_cast<int64_t>(rows) * heads * quads;
@@ -312,6 +322,8 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv
                                  int ld_src, const int32_t* __restrict__ slot_mapping, int rows, int heads,
                                  int head_dim, int block_size, __nv_bfloat16* __restrict__ kcache,
                                  __nv_bfloat16* __restrict__ vcache) {
+  pdl_trigger();
+  pdl_wait();
   const int vec_per_row = heads * head_dim / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -335,6 +347,8 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int ld_src,
                                    const int32_t* __restrict__ index, int rows, int cols,
                                    __nv_bfloat16* __restrict__ dst, int ld_dst) {
+  pdl_trigger();
+  pdl_wait();
   const int vec_per_row = cols / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -359,6 +373,8 @@ AG_DEVICE void argmax_merge(float& v, int& i, float ov, int oi) {
 __global__ void __launch_bounds__(kArgmaxThreads)
     argmax_kernel(const float* __restrict__ logits, int cols, int ld, int index_offset,
                   float* __restrict__ out_val, int32_t* __restrict__ out_idx) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * ld;
@@ -396,6 +412,8 @@ __global__ void __launch_bounds__(kArgmaxThreads)
 
 __global__ void argmax_merge_kernel(const float* __restrict__ vals, const int32_t* __restrict__ idx, int tp,
                                     int rows, int32_t* __restrict__ out_idx) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   float b = vals[r];
@@ -407,6 +425,8 @@ __global__ void argmax_merge_kernel(const float* __restrict__ vals, const int32_
 __global__ void block_copy_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                   const int32_t* __restrict__ block_ids, int n_blocks, int64_t block_elems,
                                   int gather) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t vec_per_block = block_elems / 8;
   const int64_t total = vec_per_block * n_blocks;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -437,7 +457,7 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __n
                          int max_pos_rows, __nv_bfloat16* out, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   const int64_t work = static_cast<int64_t>(rows) * (hidden / 8);
-  embed_kernel<<<grid_for(work, 256), 256, 0, stream>>>(ids, positions, tok_emb, pos_emb, pos_offset, rows,
+  (void)launch_k(kPdlOther, embed_kernel, grid_for(work, 256), 256, 0, stream, ids, positions, tok_emb, pos_emb, pos_offset, rows,
                                                         hidden, vocab, max_pos_rows, out);
   return cudaGetLastError();
 }
@@ -449,11 +469,11 @@ cudaError_t launch_layernorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const
   if (hidden % 8 != 0 || hidden / 8 > kLNThreads * kLNMaxVec) return cudaErrorInvalidValue;
   if (hidden / 8 <= 1024 * kLNVpt) {
     const int threads = ((hidden / 8 + kLNVpt - 1) / kLNVpt + 31) / 32 * 32;
-    layernorm_row_kernel<const __nv_bfloat16><<<rows, threads, 0, stream>>>(x, delta, delta_bias, row_index, gamma,
+    (void)launch_k(kPdlNorm, layernorm_row_kernel<const __nv_bfloat16>, rows, threads, 0, stream, x, delta, delta_bias, row_index, gamma,
                                                                            beta, eps, hidden, out);
     return cudaGetLastError();
   }
-  layernorm_kernel<<<rows, kLNThreads, 0, stream>>>(x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
+  (void)launch_k(kPdlNorm, layernorm_kernel, rows, kLNThreads, 0, stream, x, delta, delta_bias, row_index, gamma, beta, eps, hidden,
                                                     out);
   return cudaGetLastError();
 }
@@ -464,7 +484,7 @@ cudaError_t launch_layernorm_acc(__nv_bfloat16* x, float* acc32, const __nv_bflo
   if (rows <= 0) return cudaSuccess;
   if (hidden % 8 != 0 || hidden / 8 > 1024 * kLNVpt || acc32 == nullptr) return cudaErrorInvalidValue;
   const int threads = ((hidden / 8 + kLNVpt - 1) / kLNVpt + 31) / 32 * 32;
-  layernorm_row_kernel<float><<<rows, threads, 0, stream>>>(x, acc32, delta_bias, row_index, gamma, beta, eps, hidden,
+  (void)launch_k(kPdlNorm, layernorm_row_kernel<float>, rows, threads, 0, stream, x, acc32, delta_bias, row_index, gamma, beta, eps, hidden,
                                                             out);
   return cudaGetLastError();
 }
@@ -473,7 +493,7 @@ cudaError_t launch_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* delta, const _
                            int rows, int hidden, __nv_bfloat16* out, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (hidden % 8 != 0 || hidden / 8 > 32 * kLNWarpVec) return cudaErrorInvalidValue;
-  rmsnorm_warp_kernel<<<(rows + kLNWarpsPerBlock - 1) / kLNWarpsPerBlock, kLNWarpsPerBlock * 32, 0, stream>>>(
+  (void)launch_k(kPdlNorm, rmsnorm_warp_kernel, (rows + kLNWarpsPerBlock - 1) / kLNWarpsPerBlock, kLNWarpsPerBlock * 32, 0, stream, 
       x, delta, gamma, eps, rows, hidden, out);
   return cudaGetLastError();
 }
@@ -484,7 +504,7 @@ cudaError_t launch_rope(__nv_bfloat16* x, int ld, const int32_t* positions, int 
   if (rotary_dim % 8 != 0 || rotary_dim > head_dim || ld % 4 != 0 || head_dim % 4 != 0 || theta <= 1.0f)
     return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(rows) * heads * (rotary_dim / 8);
-  rope_kernel<<<grid_for(work, 256), 256, 0, stream>>>(x, ld, positions, rows, heads, head_dim, rotary_dim,
+  (void)launch_k(kPdlOther, rope_kernel, grid_for(work, 256), 256, 0, stream, x, ld, positions, rows, heads, head_dim, rotary_dim,
                                                         log2f(theta));
   return cudaGetLastError();
 }
@@ -495,7 +515,7 @@ cudaError_t launch_kv_append(const __nv_bfloat16* k, const __nv_bfloat16* v, int
   if (rows <= 0) return cudaSuccess;
   if (head_dim % 8 != 0 || ld_src % 8 != 0) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(rows) * heads * head_dim / 8;
-  kv_append_kernel<<<grid_for(work, 256), 256, 0, stream>>>(k, v, ld_src, slot_mapping, rows, heads, head_dim,
+  (void)launch_k(kPdlOther, kv_append_kernel, grid_for(work, 256), 256, 0, stream, k, v, ld_src, slot_mapping, rows, heads, head_dim,
                                                             block_size, kcache, vcache);
   return cudaGetLastError();
 }
@@ -504,7 +524,7 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, int ld_src, const int32
                                __nv_bfloat16* dst, int ld_dst, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   const int64_t work = static_cast<int64_t>(rows) * (cols / 8);
-  gather_rows_kernel<<<grid_for(work, 256), 256, 0, stream>>>(src, ld_src, index, rows, cols, dst, ld_dst);
+  (void)launch_k(kPdlOther, gather_rows_kernel, grid_for(work, 256), 256, 0, stream, src, ld_src, index, rows, cols, dst, ld_dst);
   return cudaGetLastError();
 }
 
@@ -512,14 +532,14 @@ cudaError_t launch_argmax(const float* logits, int rows, int cols, int ld, int i
                           int32_t* out_idx, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (ld % 4 != 0) return cudaErrorInvalidValue;
-  argmax_kernel<<<rows, kArgmaxThreads, 0, stream>>>(logits, cols, ld, index_offset, out_val, out_idx);
+  (void)launch_k(kPdlOther, argmax_kernel, rows, kArgmaxThreads, 0, stream, logits, cols, ld, index_offset, out_val, out_idx);
   return cudaGetLastError();
 }
 
 cudaError_t launch_argmax_merge(const float* vals, const int32_t* idx, int tp, int rows, int32_t* out_idx,
                                 cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
-  argmax_merge_kernel<<<(rows + 127) / 128, 128, 0, stream>>>(vals, idx, tp, rows, out_idx);
+  (void)launch_k(kPdlOther, argmax_merge_kernel, (rows + 127) / 128, 128, 0, stream, vals, idx, tp, rows, out_idx);
   return cudaGetLastError();
 }
 
@@ -528,7 +548,7 @@ cudaError_t launch_block_copy(const __nv_bfloat16* src, __nv_bfloat16* dst, cons
   if (n_blocks <= 0) return cudaSuccess;
   if (block_elems % 8 != 0) return cudaErrorInvalidValue;
   const int64_t work = block_elems / 8 * n_blocks;
-  block_copy_kernel<<<grid_for(work, 256), 256, 0, stream>>>(src, dst, block_ids, n_blocks, block_elems,
+  (void)launch_k(kPdlOther, block_copy_kernel, grid_for(work, 256), 256, 0, stream, src, dst, block_ids, n_blocks, block_elems,
                                                              gather ? 1 : 0);
   return cudaGetLastError();
 }

@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // dependents may launch only once this CTA holds its TMEM: an early dependent CTA on this SM
+  // that allocated first would wait (griddepcontrol.wait) on us while we wait on its columns
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -223,13 +226,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
+      // The weight k-blocks of the first S stages do not depend on the predecessor kernel: issue
+      // them before griddepcontrol.wait, so the weight stream starts while the predecessor drains.
+      int pre = 0;
+      {
+        SegIter ip = it;
+        while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
+          for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
+            mbar_arrive_expect_tx(&full_bar[pre], Cfg::kStageBytes);
+            tma_load_2d_hint(sB + pre * Cfg::kBBytes, &tmap_b, &full_bar[pre], kb * kBK, n_blk * BN, pol_w);
+          }
+      }
+      pdl_wait();
+      int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
-          tma_load_2d_hint(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM, pol_a);
-          tma_load_2d_hint(sB + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage], kb * kBK, n_blk * BN,
-                           pol_w);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          if (g < pre) {  // B already in flight on this stage's barrier
+            tma_load_2d_hint(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM, pol_a);
+          } else {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+            tma_load_2d_hint(sA + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kBK, m_blk * kBM, pol_a);
+            tma_load_2d_hint(sB + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage], kb * kBK, n_blk * BN, pol_w);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -274,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> fused ops -> global
     const int ew = warp - 4;
+    pdl_wait();  // the epilogue reads residuals and writes outputs the predecessor may still use
     int acc = 0;
     uint32_t acc_phase = 0;
     SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
@@ -373,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see the 1-CTA kernel)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -384,13 +405,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(M, N, K, 256, BN, k_splits, pair, num_pairs);
+      int pre = 0;  // weight k-blocks issued before griddepcontrol.wait (see the 1-CTA kernel)
+      {
+        SegIter ip = it;
+        while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
+          for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[pre], 2 * Cfg::kStageBytes);
+            tma_load_2d_cg2(sB + pre * Cfg::kBBytes, &tmap_b, full0 + pre * 8, kb * kBK, n_blk * BN + rank * (BN / 2),
+                            pol_w);
+          }
+      }
+      pdl_wait();
+      int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const uint32_t fb = full0 + stage * 8;
+          if (g >= pre) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+            tma_load_2d_cg2(sB + stage * Cfg::kBBytes, &tmap_b, fb, kb * kBK, n_blk * BN + rank * (BN / 2), pol_w);
+          }
           tma_load_2d_cg2(sA + stage * Cfg::kABytes, &tmap_a, fb, kb * kBK, m_blk * 256 + rank * 128, pol_a);
-          tma_load_2d_cg2(sB + stage * Cfg::kBBytes, &tmap_b, fb, kb * kBK, n_blk * BN + rank * (BN / 2), pol_w);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -433,6 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256-row tile
     const int ew = warp - 4;
+    pdl_wait();
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -480,6 +516,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // flight per thread).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M,
                                                             int N, GemmEpilogue ep) {
+  pdl_trigger();
+  pdl_wait();
   const int groups = N / 8;
   const int64_t total = static_cast<int64_t>(M) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -510,6 +548,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
 // Stream-K finish for GEMMs whose epilogue cannot be deferred to a consumer (QKV, FC1): the atomic
 // fp32 accumulator acc[M, N] gets the fused epilogue (8 columns per thread) and is re-zeroed.
 __global__ void __launch_bounds__(256) splitk_finish_kernel(float* __restrict__ acc, int M, int N, GemmEpilogue ep) {
+  pdl_trigger();
+  pdl_wait();
   const int groups = N / 8;
   const int64_t total = static_cast<int64_t>(M) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -587,12 +627,12 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (units < grid) grid = static_cast<int>(units);
-  gemm_bf16_tn_kernel<BN, AM><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
+  (void)launch_k(kPdlGemm, gemm_bf16_tn_kernel<BN, AM>, grid, kThreads, Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
+  (void)launch_k(kPdlGemm, splitk_reduce_kernel, rg, 256, 0, stream, partial, k_splits, M, N, ep);
   return cudaGetLastError();
 }
 
@@ -613,12 +653,12 @@ static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   int grid = num_sms() & ~1;
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas & ~1;
   if (2 * units < grid) grid = static_cast<int>(2 * units);
-  gemm2_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, M, N, K, ep, k_splits, partial);
+  (void)launch_k(kPdlGemm, gemm2_bf16_tn_kernel<BN>, grid, kThreads, Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  splitk_reduce_kernel<<<rg, 256, 0, stream>>>(partial, k_splits, M, N, ep);
+  (void)launch_k(kPdlGemm, splitk_reduce_kernel, rg, 256, 0, stream, partial, k_splits, M, N, ep);
   return cudaGetLastError();
 }
 
@@ -658,7 +698,7 @@ cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& e
   if (N % 8 != 0 || ep.mode == kEpiAtomicF32) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   const int g = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  splitk_finish_kernel<<<g, 256, 0, stream>>>(acc, M, N, ep);
+  (void)launch_k(kPdlGemm, splitk_finish_kernel, g, 256, 0, stream, acc, M, N, ep);
   return cudaGetLastError();
 }
 

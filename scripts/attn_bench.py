@@ -61,6 +61,9 @@ def run(seqs, heads):
     for _ in range(10):
         flush.zero_()  # L2 flush between timed launches
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        # keep the device busy while the host builds the work list, so the events bracket device
+        # time only (as in the forward, where the list is built while earlier kernels run)
+        torch.cuda._sleep(1_000_000)
         e0.record()
         K.paged_attention(q, kp, vp, btd, cu, ctx, out=out, workspace=ws, device_meta=meta)
         e1.record()

@@ -39,6 +39,12 @@ constexpr int kQOff = 0;                            // Q: 2 sub-tiles (dims 0-63
 constexpr int kKVOff = 2 * kSub;                    // stage s: K 2 sub-tiles, V 2 sub-tiles (64 KB)
 constexpr int kStageBytes = 4 * kSub;
 constexpr int kKVStages = 3;                        // P lives in TMEM, so three K/V stages fit
+#ifndef AG_ATTN_SBUF
+#define AG_ATTN_SBUF 3
+#endif
+constexpr int kSBuf = AG_ATTN_SBUF;                 // S/P buffers in TMEM (128 columns each)
+constexpr uint32_t kOCol = kSBuf * 128;             // O accumulator columns
+static_assert(kSBuf * 128 + 128 <= 512, "TMEM: S buffers + O must fit 512 columns");
 constexpr int kBarOff = kKVOff + kKVStages * kStageBytes;  // 224 KB
 constexpr int kTileSmem = kBarOff + 256;
 // ---- row path layout (per warp): kRowStages pages of 32 tokens; a stage is
@@ -263,8 +269,8 @@ AG_DEVICE void decode_row_warp(const AttnParams& p, const AttnTmaps& tm, const A
 struct TileBars {
   uint64_t q_full;
   uint64_t kv_full[kKVStages], kv_empty[kKVStages];
-  uint64_t s_full[2], s_empty[2];
-  uint64_t p_full[2], o_done[2];
+  uint64_t s_full[kSBuf], s_empty[kSBuf];
+  uint64_t p_full[kSBuf], o_done[2];
   uint32_t tmem_base;
 };
 
@@ -275,15 +281,19 @@ struct TileBars {
 #endif
 
 #ifdef AG_ATTN_TIMELINE  // timing probe only: per-CTA globaltimer stamps (entry, setup, loop end, exit)
-__device__ unsigned long long g_attn_tl[16384 * 6];
+__device__ unsigned long long g_attn_tl[16384 * 16];
 AG_DEVICE unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define AG_TL(slot, v) g_attn_tl[blockIdx.x * 6 + (slot)] = (v)
+#define AG_TL(slot, v) g_attn_tl[blockIdx.x * 16 + (slot)] = (v)
+#define AG_CLK(var) const long long var = clock64()
+#define AG_ACC(var, v) var += (v)
 #else
 #define AG_TL(slot, v)
+#define AG_CLK(var)
+#define AG_ACC(var, v)
 #endif
 
 AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem& it, int head, uint8_t* smem) {
@@ -312,12 +322,12 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSBuf; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_empty[i], 4);
       mbar_init(&bars->p_full[i], 4);
-      mbar_init(&bars->o_done[i], 1);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(&bars->o_done[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
@@ -329,7 +339,7 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #endif
   pdl_trigger();  // only after the TMEM allocation (see gemm_bf16_tn_kernel)
   pdl_wait();     // Q, the paged K/V and the outputs belong to the predecessor kernels
-  const uint32_t tmem = bars->tmem_base;  // S0 [0,128) S1 [128,256) O [256,384)
+  const uint32_t tmem = bars->tmem_base;  // S buffers [128 i, 128 i + 128), O [kOCol, kOCol + 128)
 
   if (warp == 0) {
     if (lane == 0 && n_tiles > 0) {
@@ -341,9 +351,13 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
       tma_load_2d(smem + kQOff + kSub, &tm.q, &bars->q_full, head * kHD + 64, tok_row0);
       const int32_t* bt = p.block_table + static_cast<int64_t>(it.seq) * p.bt_stride;
       const int last_page = (kv_end - 1) / kPage;
+      long long c_ke = 0;
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % kKVStages;
+        AG_CLK(e0);
         mbar_wait(&bars->kv_empty[st], ((j / kKVStages) & 1) ^ 1);
+        AG_CLK(e1);
+        AG_ACC(c_ke, e1 - e0);
 #ifdef AG_ATTN_PROBE_NOTMA  // timing probe only: K/V stages are not loaded (MMAs read stale smem)
         mbar_arrive(&bars->kv_full[st]);
         continue;
@@ -361,16 +375,23 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
           tma_load_2d(vdst + kSub + pg * 4096, &tm.v, &bars->kv_full[st], 64, row);
         }
       }
+      AG_TL(13, c_ke);
     }
   } else if (warp == 1) {
     if (lane == 0 && n_tiles > 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(kTM, kTN);
       constexpr uint32_t idesc_o = umma_idesc_bf16(kTM, kHD) | (1u << 16);  // B (V) MN-major
       mbar_wait(&bars->q_full, 0);
+      long long c_kv = 0, c_se = 0, c_pf = 0;
       auto issue_s = [&](int j) {
-        const int st = j % kKVStages, sbuf = j & 1;
+        const int st = j % kKVStages, sbuf = j % kSBuf;
+        AG_CLK(k0);
         mbar_wait(&bars->kv_full[st], (j / kKVStages) & 1);
-        mbar_wait(&bars->s_empty[sbuf], ((j >> 1) & 1) ^ 1);
+        AG_CLK(k1);
+        mbar_wait(&bars->s_empty[sbuf], ((j / kSBuf) & 1) ^ 1);
+        AG_CLK(k2);
+        AG_ACC(c_kv, k1 - k0);
+        AG_ACC(c_se, k2 - k1);
         tc_fence_after();
         const uint32_t kaddr = sb + kKVOff + st * kStageBytes;
 #ifndef AG_ATTN_PROBE_NOS  // timing probe only: skip the S MMAs
@@ -383,25 +404,42 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #endif
         umma_commit(&bars->s_full[sbuf]);
       };
-      issue_s(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s(j + 1);
-        const int pb = j & 1, st = j % kKVStages;
-        AG_TILE_WAIT(&bars->p_full[pb], (j >> 1) & 1);
+      // O += P_j . V_j with P_j (bf16, packed in columns 0-63 of its S buffer) as the TMEM A operand
+      auto issue_pv = [&](int j) {
+        const int pb = j % kSBuf, st = j % kKVStages;
+        AG_CLK(p0);
+        AG_TILE_WAIT(&bars->p_full[pb], (j / kSBuf) & 1);
+        AG_CLK(p1);
+        AG_ACC(c_pf, p1 - p0);
         tc_fence_after();
-        // O += P_j . V_j with P_j (bf16, packed in columns 0-63 of S buffer pb) as the TMEM A operand
         const uint32_t ptmem = tmem + pb * 128;
         const uint32_t vaddr = sb + kKVOff + st * kStageBytes + 2 * kSub;
 #ifndef AG_ATTN_PROBE_NOPV  // timing probe only: skip the P.V MMAs
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA = 8 TMEM columns of packed bf16 pairs
           const uint64_t b = umma_desc_sw128_mn(vaddr + k * 2048, kSub);
-          umma_bf16_ts(tmem + 256, ptmem + 8 * k, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + kOCol, ptmem + 8 * k, b, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
 #endif
-        umma_commit(&bars->o_done[pb]);
+        umma_commit(&bars->o_done[j & 1]);
         umma_commit(&bars->kv_empty[st]);
+      };
+      if constexpr (kSBuf == 2) {  // S_{j+1} is queued before P_j is awaited
+        issue_s(0);
+        for (int j = 0; j < n_tiles; ++j) {
+          if (j + 1 < n_tiles) issue_s(j + 1);
+          issue_pv(j);
+        }
+      } else {  // S_{j+1}, S_{j+2} run ahead: the softmax never waits for S on the S -> P -> PV loop
+        for (int j = 0; j < kSBuf - 1 && j < n_tiles; ++j) issue_s(j);
+        for (int j = 0; j < n_tiles; ++j) {
+          issue_pv(j);
+          if (j + kSBuf - 1 < n_tiles) issue_s(j + kSBuf - 1);
+        }
       }
+      AG_TL(10, c_pf);
+      AG_TL(11, c_kv);
+      AG_TL(12, c_se);
     }
   } else {
     // ---------------- softmax / epilogue warps: one query row per thread
@@ -411,16 +449,20 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
     const bool row_ok = row < it.q_rows;
     const int qpos = ctx + it.q_start + row;
     float m_used = -INFINITY, l = 0.f;
+    long long c_w = 0, c_ld = 0, c_mx = 0, c_ex = 0;
     for (int j = 0; j < n_tiles; ++j) {
-      const int sbuf = j & 1;
-      AG_TILE_WAIT(&bars->s_full[sbuf], (j >> 1) & 1);
+      const int sbuf = j % kSBuf;
+      AG_CLK(t0);
+      AG_TILE_WAIT(&bars->s_full[sbuf], (j / kSBuf) & 1);
       tc_fence_after();
+      AG_CLK(t1);
+      AG_ACC(c_w, t1 - t0);
 #ifdef AG_ATTN_PIPE_PROBE  // timing probe only: skip the softmax, keep the barrier protocol
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&bars->s_empty[sbuf]);
-        mbar_arrive(&bars->p_full[j & 1]);
+        mbar_arrive(&bars->p_full[sbuf]);
       }
       continue;
 #endif
@@ -428,14 +470,21 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
+#ifdef AG_ATTN_PROBE_NOLDS  // timing probe only: S not read from TMEM (synthetic scores)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(0.01f * (lane ^ (c * 32 + i)) + 0.001f * j);
+#else
         tmem_ld_32x32b_x32(tmem + lane_addr + sbuf * 128 + c * 32, r);
         tmem_ld_wait();
+#endif
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->s_empty[sbuf]);
+      AG_CLK(t2);
+      AG_ACC(c_ld, t2 - t1);
       const int kbase = it.kv_start + j * kTN;
       // Only the tiles that cross a row's causal / range end need a mask (CTA-uniform test on
       // row 0, the row with the earliest end); rows past q_rows are never stored.
@@ -444,9 +493,12 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = c < lim ? s[c] : -INFINITY;
       }
-      float mx = -INFINITY;
+      float m8[8];  // 8 independent max chains (a single 128-long fmax chain is latency-bound)
 #pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      for (int i = 0; i < 8; ++i) m8[i] = s[i];
+#pragma unroll
+      for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       mx *= kLog2e;  // scores stay raw; the log2(e) scale is folded into the exponent's FMA
       // Lazy rescale: a row whose running max grew by more than 2^8 rescales l and its O row
       // (after every earlier P.V finished).  tcgen05.ld/st are .sync.aligned, so the decision to
@@ -460,11 +512,11 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+            tmem_ld_32x32b_x32(tmem + lane_addr + kOCol + c * 32, r);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+            tmem_st_32x32b_x32(tmem + lane_addr + kOCol + c * 32, r);
           }
           tmem_st_wait();
           tc_fence_before();
@@ -475,31 +527,44 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
         }
       }
       const float mref = m_used == -INFINITY ? 0.f : m_used;
+      AG_CLK(t3);
+      AG_ACC(c_mx, t3 - t2);
       // P_j (bf16 pairs) -> columns 0-63 of this tile's S buffer; S_j is already in registers and
       // the MMA pipe runs P.V_j before the S_{j+2} that next overwrites the buffer (in-order issue)
-      float rs = 0.f;
+      float rs2[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial row sums
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
+#ifdef AG_ATTN_PROBE_NOEXP  // timing probe only: no MUFU (values are wrong)
+          const float e0 = fmaf(s[half * 64 + 2 * i], kLog2e, -mref);
+          const float e1 = fmaf(s[half * 64 + 2 * i + 1], kLog2e, -mref);
+#else
           const float e0 = ex2_ftz(fmaf(s[half * 64 + 2 * i], kLog2e, -mref));
           const float e1 = ex2_ftz(fmaf(s[half * 64 + 2 * i + 1], kLog2e, -mref));
-          rs += e0 + e1;
+#endif
+          rs2[i & 3] += e0 + e1;
           pk[i] = pack_bf16x2(e0, e1);
         }
         tmem_st_32x32b_x32(tmem + lane_addr + sbuf * 128 + half * 32, pk);
       }
       tmem_st_wait();
-      l += rs;
+      l += (rs2[0] + rs2[1]) + (rs2[2] + rs2[3]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&bars->p_full[sbuf]);
+      AG_CLK(t4);
+      AG_ACC(c_ex, t4 - t3);
     }
 #ifdef AG_ATTN_TIMELINE
     if (threadIdx.x == 64) {
       AG_TL(2, gtimer());
       AG_TL(4, n_tiles);
+      AG_TL(6, c_w);
+      AG_TL(7, c_ld);
+      AG_TL(8, c_mx);
+      AG_TL(9, c_ex);
     }
 #endif
     // epilogue: O row / l
@@ -512,7 +577,7 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
     for (int c = 0; c < 4; ++c) {
       uint32_t r[32];
       if (n_tiles > 0) {
-        tmem_ld_32x32b_x32(tmem + lane_addr + 256 + c * 32, r);
+        tmem_ld_32x32b_x32(tmem + lane_addr + kOCol + c * 32, r);
         tmem_ld_wait();
       } else {
 #pragma unroll
@@ -614,7 +679,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(AttnParams p, const A
 
 #ifdef AG_ATTN_TIMELINE
 extern "C" __attribute__((visibility("default"))) int ag_debug_attn_timeline(void* dst, int n) {
-  return static_cast<int>(cudaMemcpyFromSymbol(dst, g_attn_tl, sizeof(unsigned long long) * 6 * n));
+  return static_cast<int>(cudaMemcpyFromSymbol(dst, g_attn_tl, sizeof(unsigned long long) * 16 * n));
 }
 #endif
 

@@ -1017,12 +1017,12 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         ea.acc32 = m->acc_big;
         ea.ldc = sh.N;
         const ag::GemmEpilogue& eg = finish ? ea : ep;
-        if (p.am == 256 && (p.bn == 64 || M < 256)) continue;  // CTA pair: bn 128/256, M >= 256
+        if (p.am == 256 && (p.bn == 64 || M <= 128)) continue;  // CTA pair: bn 128/256, M > 128
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.bn == 160 && (!sh.w[0]->has160 || p.am == 256)) continue;
         if (p.am < 128 && M > p.am) continue;
         if (p.k_splits == ag::kStreamK) {
-          if (k == kGemmLm || (p.am == 256 && M < 256)) continue;
+          if (k == kGemmLm || (p.am == 256 && M <= 128)) continue;
           if ((k == kGemmOut || k == kGemmFc2) && c.tp_size != 1) continue;
         } else {
           const int nkb = (sh.K + 63) / 64, per = (nkb + p.k_splits - 1) / p.k_splits;

@@ -21,10 +21,10 @@ r = attn_bench.run(seqs, 40)
 lib = _lib.load()
 fn = lib.ag_debug_attn_timeline
 n = 16384
-buf = (ctypes.c_ulonglong * (6 * n))()
+buf = (ctypes.c_ulonglong * (16 * n))()
 torch.cuda.synchronize()
 assert fn(ctypes.cast(buf, ctypes.c_void_p), n) == 0
-rows = [tuple(buf[6 * i:6 * i + 6]) for i in range(n)]
+rows = [tuple(buf[16 * i:16 * i + 16]) for i in range(n)]
 rows = [x for x in rows if x[0] and x[3] >= x[0]]
 t0 = min(x[0] for x in rows)
 last = max(x[3] for x in rows)
@@ -49,3 +49,8 @@ print("per-tile us", q(per_tile), "tiles/CTA", q([x[4] for x in rows]))
 if gaps:
     print("gap between CTAs on an SM us", q(gaps))
 print("first-wave start spread us", f"{starts[min(len(starts) - 1, 147)]:.2f}")
+tiles = sum(x[4] for x in rows)
+names = {6: "softmax wait S", 7: "softmax load S", 8: "softmax max/rescale", 9: "softmax exp/store P",
+         10: "mma wait P", 11: "mma wait K/V", 12: "mma wait S-empty", 13: "producer wait stage"}
+for k, nm in names.items():
+    print(f"{nm:22s} {sum(x[k] for x in rows) / max(tiles, 1):8.0f} cycles/tile")

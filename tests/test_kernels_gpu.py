@@ -208,6 +208,8 @@ def test_mixed_attention(K, seqs, heads):
     ([(0, 1000)], 40),
     # chunk whose causal end is inside the first KV tile of a split
     ([(12000, 130), (7, 3)], 2),
+    # many more (tile item, head) units than SMs: persistent tile CTAs run several units each
+    ([(0, 512)] * 6 + [(3000, 300), (9000, 1), (0, 40)], 24),
 ])
 def test_mixed_attention_boundaries(K, seqs, heads):
     q, kp, vp, bt, cu, ctx = _attn_case(seqs, heads, seed=sum(c + n for c, n in seqs) % 997)
@@ -216,6 +218,19 @@ def test_mixed_attention_boundaries(K, seqs, heads):
     ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
     err = (out.float().cpu() - ref).abs().max().item()
     assert err <= 2e-2, err
+
+
+def test_mixed_attention_back_to_back(K):
+    """Persistent tile CTAs take units from a device counter that the last CTA of each launch
+    resets: consecutive launches of different shapes must each cover all their units."""
+    cases = [([(0, 700)] * 3, 40), ([(2000, 129), (0, 5)], 40), ([(0, 700)] * 3, 40)]
+    for seqs, heads in cases:
+        q, kp, vp, bt, cu, ctx = _attn_case(seqs, heads, seed=11)
+        out = K.paged_attention(q.to(DEV), kp.to(DEV), vp.to(DEV), bt.to(DEV), cu, ctx)
+        torch.cuda.synchronize()
+        ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
+        err = (out.float().cpu() - ref).abs().max().item()
+        assert err <= 2e-2, (seqs[:2], err)
 
 
 def test_kv_swap_roundtrip(K):

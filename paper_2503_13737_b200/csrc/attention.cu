@@ -625,16 +625,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int n_tile_ctas = n_tile_items * p.heads;
-  if (static_cast<int>(blockIdx.x) < n_tile_ctas) {
+  // The tile CTAs (tensor-bound) are spread evenly through the grid, tile i at block
+  // floor(i * C / T), so they run concurrently with the HBM-bound decode-row CTAs from the first
+  // wave on instead of occupying the SMs ahead of them.
+  const long long C = gridDim.x, T = n_tile_ctas, b = blockIdx.x;
+  const long long ti = T > 0 ? (b * T + C - 1) / C : 0;  // the only tile index that can sit at b
+  if (ti < T && ti * C / T == b) {
     // head-major: the q tiles / splits of one head run side by side and share its K/V in L2
-    const AttnItem it = items[blockIdx.x % n_tile_items];
-    tile_tc(p, tm, it, blockIdx.x / n_tile_items, smem);
+    const AttnItem it = items[ti % n_tile_items];
+    tile_tc(p, tm, it, static_cast<int>(ti / n_tile_items), smem);
     return;
   }
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5;
-  const int u = (blockIdx.x - n_tile_ctas) * (kThreads / 32) + warp;
+  const int row_cta = static_cast<int>(b - (T > 0 ? ((b + 1) * T + C - 1) / C : 0));  // tiles at or before b
+  const int u = row_cta * (kThreads / 32) + warp;
   if (u >= n_row_items * p.heads) return;
   const AttnItem itr = items[n_tile_items + u / p.heads];
   decode_row_warp(p, tm, itr, u % p.heads, smem + warp * kRowWarpBytes,

@@ -111,7 +111,9 @@ AG_API int32_t ag_device_sm_count(void);
 /* ---- model lifecycle (reference boundary: engine.step's clock advance) ---- */
 /* Environment: AG_DETERMINISTIC=1 (read at create) disables the fp32-atomic split-K / stream-K
  * epilogues, so every result is bitwise reproducible run to run; AG_DEBUG_SYNC=1 synchronises and
- * checks after every launch of the forward. */
+ * checks after every launch of the forward; AG_PDL=0 launches the forward's kernels without
+ * programmatic dependent launch (default on: a kernel's prologue and weight prefetch overlap its
+ * predecessor's tail; AG_PDL_MASK=<bits> per launch class, see common.cuh). */
 AG_API int32_t ag_model_create(const ag_model_config* cfg, ag_model** out);
 AG_API void ag_model_destroy(ag_model* m);
 AG_API int32_t ag_model_set_embeddings(ag_model* m, const void* tok_emb /*[V,H]*/, const void* pos_emb /*[pos_rows,H]*/,

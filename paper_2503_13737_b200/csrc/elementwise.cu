@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(kLNThreads)
                      const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
                      const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
                      float eps, int hidden, __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();  // after the wait: an early norm never lets a third kernel in
   __shared__ float red[kLNThreads / 32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(1024)
                          const __nv_bfloat16* __restrict__ delta_bias, const int32_t* __restrict__ row_index,
                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
                          float eps, int hidden, __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();  // after the wait: an early norm never lets a third kernel in
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
     rmsnorm_warp_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                         const __nv_bfloat16* __restrict__ gamma, float eps, int rows, int hidden,
                         __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();  // after the wait: an early norm never lets a third kernel in
   const int r = blockIdx.x * kLNWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= rows) return;
   const int lane = threadIdx.x & 31;

@@ -151,6 +151,10 @@ void build_attention_work(const int32_t* cu_q, const int32_t* ctx_len, int B, in
       emit(t, n, sp, row_items);
     }
   }
+  // longest decode pieces first: the short ones fill the last wave instead of trailing it
+  std::stable_sort(row_items.begin(), row_items.end(), [](const AttnItem& a, const AttnItem& b) {
+    return a.kv_end - a.kv_start > b.kv_end - b.kv_start;
+  });
   w.n_tile = static_cast<int>(tile_items.size());
   w.n_row = static_cast<int>(row_items.size());
   w.items = std::move(tile_items);

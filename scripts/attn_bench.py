@@ -30,6 +30,8 @@ CASES = {
     "live_dec40_fresh300": [(2200, 1)] * 40 + [(0, 300)],
     "live_dec40_chunk280_on1200": [(2200, 1)] * 40 + [(1200, 280), (0, 20)],
     "live_dec60_chunk64_on510": [(2100, 1)] * 60 + [(510, 64)],
+    "decode_var64": [(100 + (i * 977) % 4000, 1) for i in range(64)],
+    "live_var48_chunk200": [(100 + (i * 977) % 4000, 1) for i in range(48)] + [(600, 200)],
 }
 
 

@@ -1,0 +1,27 @@
+"""Programmatic dependent launch changes only when a kernel may start, never what it computes:
+the same mixed forward with AG_PDL=0 and with PDL on (default) must give bitwise-identical logits
+(AG_DETERMINISTIC=1, and one GEMM plan table shared through AG_GEMM_PLAN_CACHE so both processes
+run the same tile shapes).  The switch is read once per process, hence the subprocesses."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(out, env):
+    r = subprocess.run([sys.executable, "tests/helpers/pdl_forward.py", str(out)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(out)
+
+
+def test_pdl_on_off_bitwise(tmp_path):
+    base = dict(os.environ, AG_DETERMINISTIC="1", AG_GEMM_PLAN_CACHE=str(tmp_path / "plans"))
+    off = _run(tmp_path / "off.npy", dict(base, AG_PDL="0"))  # autotunes, writes the plan cache
+    on = _run(tmp_path / "on.npy", {k: v for k, v in base.items() if k != "AG_PDL"})  # reads it
+    assert off.shape == on.shape and off.size > 0
+    assert np.array_equal(off, on), float(np.abs(off - on).max())

@@ -58,7 +58,8 @@ def test_gemm_small_m_variant(K, M, N, K_, bn, splits, a_rows):
 
 
 @pytest.mark.parametrize("M,N,K_,bn,splits", [(256, 512, 256, 256, 1), (300, 1920, 640, 128, 1), (1000, 5120, 1024, 256, 1),
-                                              (777, 2560, 5120, 256, 2), (2048, 3072, 5120, 128, 1), (129, 768, 512, 256, 1)])
+                                              (777, 2560, 5120, 256, 2), (2048, 3072, 5120, 128, 1), (129, 768, 512, 256, 1),
+                                              (192, 2560, 5120, 256, 1), (255, 1280, 2048, 128, 1)])
 def test_gemm_cta_pair(K, M, N, K_, bn, splits):
     """CTA-pair (cta_group::2, 256-row tiles) kernel with bias + residual epilogue vs fp32."""
     a, w = _bf((M, K_), 31), _bf((N, K_), 32, 0.05)

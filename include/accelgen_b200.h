@@ -124,6 +124,21 @@ AG_API int32_t ag_model_set_kv_cache(ag_model* m, int32_t layer, void* k_pool, v
  * then every rank calls ag_model_init_tp (NCCL communicator over NVLink, in-stream all-reduce). */
 AG_API int32_t ag_nccl_get_unique_id(void* out_128_bytes);
 AG_API int32_t ag_model_init_tp(ag_model* m, const void* unique_id_128_bytes);
+/* Host collective backend (instead of ag_model_init_tp): every collective of the forward is copied
+ * D2H into a pinned staging buffer, the stream is synchronised, and `fn` completes it in place on
+ * that host buffer; the result is copied back H2D.  op AG_COLL_ALLREDUCE_SUM: `count` elements of
+ * `dtype` summed over ranks in place.  op AG_COLL_ALLGATHER: the buffer holds tp_size slots of
+ * `count` elements, this rank's slot (index tp_rank) filled; fn fills the others.  fn returns 0 on
+ * success.  Used to run several TP ranks as processes sharing ONE GPU (NCCL refuses two ranks on a
+ * device), so the sharded forward -- head-split attention, bias-after-reduce LayerNorm, the
+ * vocab-parallel argmax merge -- is testable on a single B200; not a performance path. */
+#define AG_COLL_ALLREDUCE_SUM 0
+#define AG_COLL_ALLGATHER 1
+#define AG_DT_BF16 0
+#define AG_DT_F32 1
+#define AG_DT_I32 2
+typedef int32_t (*ag_host_collective_fn)(void* ctx, int32_t op, void* host_buf, int64_t count, int32_t dtype);
+AG_API int32_t ag_model_init_tp_host(ag_model* m, ag_host_collective_fn fn, void* ctx);
 
 /* Execute one BatchPlan.  Host metadata is packed into one pinned buffer, copied H2D on
  * `stream`, the forward runs, and next-token ids are copied back into out_tokens (host, int32

@@ -36,7 +36,7 @@ class OracleExecutor:
         return StepResult(token_ids=toks.numpy(), elapsed_s=dt, device_s=dt, wall_s=dt, logits=logits)
 
     def swap_out(self, request_id, block_ids, tokens):
-        ids = torch.tensor(block_ids, dtype=torch.long)
+        ids = torch.tensor(block_ids, dtype=torch.long, device=self.model.dev)
         self._swapped[request_id] = [(k[ids].clone(), v[ids].clone())
                                      for k, v in zip(self.model.k_pools, self.model.v_pools)]
 
@@ -45,7 +45,7 @@ class OracleExecutor:
         if saved is None:
             return
         n = saved[0][0].shape[0]
-        ids = torch.tensor(block_ids[:n], dtype=torch.long)
+        ids = torch.tensor(block_ids[:n], dtype=torch.long, device=self.model.dev)
         for (k, v), kp, vp in zip(saved, self.model.k_pools, self.model.v_pools):
             kp[ids] = k
             vp[ids] = v

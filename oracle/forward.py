@@ -16,7 +16,14 @@ What it restates
 
 Rounding points mirror the device kernels: activations are stored in bf16 between kernels
 (q after scaling, K/V in the cache, attention output, residual stream, LN outputs, FC1 output);
-every matmul accumulates in fp32; softmax and LN statistics are fp32; logits stay fp32.
+every matmul accumulates in fp32; softmax and LN statistics are fp32; logits stay fp32.  In the
+attention the unnormalised probabilities exp(s - max) are rounded to bf16 before P.V, while the
+row sum l uses the fp32 values (attention.cu: pack_bf16x2 of p, l += p in fp32), then O = (P.V)/l.
+
+Device: the restatement is plain torch.  It runs on the CPU by default; the large-shape tests
+(40-layer OPT-13B, 100k-token contexts) run the SAME code on the GPU in fp32 with TF32 disabled
+(``OracleOPT(..., device="cuda")``), where a CPU run would take hours.  It is still the checker,
+never the product path.
 """
 from __future__ import annotations
 
@@ -30,6 +37,8 @@ HEAD_DIM = 128
 
 
 ROUND_BF16 = True  # False = pure fp32 restatement (used to pin against transformers' fp32 OPT)
+DEVICE = torch.device("cpu")  # where f32() materialises operands; OracleOPT switches it per forward
+ATTN_SCORE_ELEMS = 1 << 27     # heads x rows x kv_len fp32 scores held at once (query rows are chunked)
 
 
 def rb(x: torch.Tensor) -> torch.Tensor:
@@ -40,7 +49,7 @@ def rb(x: torch.Tensor) -> torch.Tensor:
 
 
 def f32(x: torch.Tensor) -> torch.Tensor:
-    return x.detach().to("cpu", torch.float32)
+    return x.detach().to(DEVICE, torch.float32)
 
 
 def embed(ids, positions, tok_emb, pos_emb):
@@ -80,7 +89,8 @@ def paged_attention(q, k_pool, v_pool, block_table, cu_q, ctx_len, block_size=32
     0..ctx_len[b]+i of the sequence's pages (causal, prefix cache included)."""
     S = q.shape[0]
     heads = k_pool.shape[1]
-    out = torch.zeros(S, heads * HEAD_DIM, dtype=torch.float32)
+    dev = q.device
+    out = torch.zeros(S, heads * HEAD_DIM, dtype=torch.float32, device=dev)
     cu_q = [int(v) for v in cu_q]
     for b in range(len(cu_q) - 1):
         q0, q1 = cu_q[b], cu_q[b + 1]
@@ -90,29 +100,33 @@ def paged_attention(q, k_pool, v_pool, block_table, cu_q, ctx_len, block_size=32
         ctx = int(ctx_len[b])
         kv_len = ctx + n_q
         n_pages = (kv_len + block_size - 1) // block_size
-        pages = block_table[b, :n_pages].long()
+        pages = block_table[b, :n_pages].long().to(k_pool.device)
         k = f32(k_pool[pages]).permute(1, 0, 2, 3).reshape(heads, n_pages * block_size, HEAD_DIM)[:, :kv_len]
         v = f32(v_pool[pages]).permute(1, 0, 2, 3).reshape(heads, n_pages * block_size, HEAD_DIM)[:, :kv_len]
-        qb = q[q0:q1].reshape(n_q, heads, HEAD_DIM).permute(1, 0, 2)
-        s = qb @ k.transpose(1, 2)  # [heads, n_q, kv_len]
-        qpos = ctx + torch.arange(n_q).unsqueeze(1)
-        kpos = torch.arange(kv_len).unsqueeze(0)
-        s = s.masked_fill(kpos > qpos, float("-inf"))
-        p = torch.softmax(s, dim=-1)
-        o = p @ v  # [heads, n_q, 128]
-        out[q0:q1] = o.permute(1, 0, 2).reshape(n_q, heads * HEAD_DIM)
+        rows = max(1, ATTN_SCORE_ELEMS // (heads * kv_len))
+        for r0 in range(0, n_q, rows):
+            r1 = min(n_q, r0 + rows)
+            qb = q[q0 + r0:q0 + r1].reshape(r1 - r0, heads, HEAD_DIM).permute(1, 0, 2)
+            hi = ctx + r1  # keys past the chunk's last query row are masked for every row of it
+            s = qb @ k[:, :hi].transpose(1, 2)  # [heads, rows, hi]
+            qpos = ctx + torch.arange(r0, r1, device=dev).unsqueeze(1)
+            kpos = torch.arange(hi, device=dev).unsqueeze(0)
+            s = s.masked_fill(kpos > qpos, float("-inf"))
+            p = torch.exp(s - s.amax(dim=-1, keepdim=True))
+            l = p.sum(dim=-1, keepdim=True)
+            o = (rb(p) @ v[:, :hi]) / l  # bf16 P into P.V, fp32 row sum (attention.cu)
+            out[q0 + r0:q0 + r1] = o.permute(1, 0, 2).reshape(r1 - r0, heads * HEAD_DIM)
     return out
 
 
 def kv_append(k_rows, v_rows, slot_mapping, k_pool, v_pool, block_size=32):
     """Write rows [S, heads*128] into their (block, offset) slots; slots < 0 are skipped."""
     heads = k_pool.shape[1]
-    for i, slot in enumerate(slot_mapping.tolist()):
-        if slot < 0:
-            continue
-        blk, off = divmod(slot, block_size)
-        k_pool[blk, :, off, :] = k_rows[i].reshape(heads, HEAD_DIM).to(k_pool.dtype)
-        v_pool[blk, :, off, :] = v_rows[i].reshape(heads, HEAD_DIM).to(v_pool.dtype)
+    slots = slot_mapping.long().to(k_pool.device)
+    keep = slots >= 0
+    blk, off = slots[keep] // block_size, slots[keep] % block_size
+    k_pool[blk, :, off, :] = k_rows[keep.to(k_rows.device)].reshape(-1, heads, HEAD_DIM).to(k_pool.device, k_pool.dtype)
+    v_pool[blk, :, off, :] = v_rows[keep.to(v_rows.device)].reshape(-1, heads, HEAD_DIM).to(v_pool.device, v_pool.dtype)
 
 
 @dataclass
@@ -131,8 +145,10 @@ class OracleOPT:
     """Paged-KV OPT forward on the CPU.  ``weights`` follows paper_2503_13737_b200.model.init_weights
     (full model, tp_size=1) or one TP shard when tp_size > 1 (then ``allreduce`` sums partials)."""
 
-    def __init__(self, cfg, weights, num_blocks, block_size=32, tp_rank=0, tp_size=1, allreduce=None):
+    def __init__(self, cfg, weights, num_blocks, block_size=32, tp_rank=0, tp_size=1, allreduce=None,
+                 device="cpu"):
         self.cfg = cfg
+        self.dev = torch.device(device)
         self.w = weights
         self.block_size = block_size
         self.tp_rank, self.tp_size = tp_rank, tp_size
@@ -140,7 +156,7 @@ class OracleOPT:
         heads_l = cfg.num_heads // tp_size
         self.heads_l = heads_l
         pool_dtype = torch.bfloat16 if ROUND_BF16 else torch.float32
-        self.k_pools = [torch.zeros(num_blocks, heads_l, block_size, HEAD_DIM, dtype=pool_dtype)
+        self.k_pools = [torch.zeros(num_blocks, heads_l, block_size, HEAD_DIM, dtype=pool_dtype, device=self.dev)
                         for _ in range(cfg.num_layers)]
         self.v_pools = [torch.zeros_like(p) for p in self.k_pools]
         self.scale = 1.0 / math.sqrt(HEAD_DIM)
@@ -151,7 +167,21 @@ class OracleOPT:
         return self.allreduce(partial)
 
     def forward(self, st: StepInputs):
+        global DEVICE
+        prev, DEVICE = DEVICE, self.dev
+        tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False  # true fp32 matmuls when run on the GPU
+        try:
+            return self._forward(st)
+        finally:
+            DEVICE = prev
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+
+    def _forward(self, st: StepInputs):
         cfg, w = self.cfg, self.w
+        dev = self.dev
+        st = StepInputs(st.token_ids.to(dev), st.positions.to(dev), st.cu_q, st.ctx_len, st.block_table,
+                        st.slot_mapping.to(dev), st.logit_rows.to(dev))
         hq = self.heads_l * HEAD_DIM
         x = embed(st.token_ids, st.positions, w["tok_emb"], w["pos_emb"])
         for l, L in enumerate(w["layers"]):
@@ -178,4 +208,4 @@ class OracleOPT:
         rows = st.logit_rows.long()
         hl = layernorm(x[rows], w["final_g"], w["final_b"], cfg.ln_eps)
         logits = hl @ f32(w["tok_emb"]).T
-        return logits, torch.argmax(logits, dim=-1).to(torch.int32)
+        return logits.cpu(), torch.argmax(logits, dim=-1).to(torch.int32).cpu()

@@ -28,6 +28,12 @@ P_i32 = C.POINTER(C.c_int32)
 P_f32 = C.POINTER(C.c_float)
 
 
+# ag_host_collective_fn (include/accelgen_b200.h): (ctx, op, host_buf, count, dtype) -> 0 on success
+HOST_COLLECTIVE_FN = C.CFUNCTYPE(i32, vp, i32, vp, i64, i32)
+COLL_ALLREDUCE_SUM, COLL_ALLGATHER = 0, 1
+DT_BF16, DT_F32, DT_I32 = 0, 1, 2
+
+
 class ModelConfig(C.Structure):
     _fields_ = [("hidden", i32), ("num_layers", i32), ("num_heads", i32), ("ffn", i32), ("vocab", i32),
                 ("pos_rows", i32), ("tp_rank", i32), ("tp_size", i32), ("num_blocks", i32),
@@ -57,6 +63,7 @@ _SIGS = {
     "ag_model_set_kv_cache": (i32, [vp, i32, vp, vp]),
     "ag_nccl_get_unique_id": (i32, [vp]),
     "ag_model_init_tp": (i32, [vp, vp]),
+    "ag_model_init_tp_host": (i32, [vp, vp, vp]),
     "ag_model_forward": (i32, [vp, C.POINTER(Step), vp, vp, P_f32, vp]),
     "ag_model_stage_step": (i32, [vp, C.POINTER(Step), vp]),
     "ag_model_forward_staged": (i32, [vp, vp, vp, vp]),

@@ -442,6 +442,24 @@ __global__ void block_copy_kernel(const __nv_bfloat16* __restrict__ src, __nv_bf
   }
 }
 
+// Deterministic pseudo-random bf16 fill: x = scale * u (or max(0, scale * u) with relu),
+// u ~ U[-1, 1) from a hash of (seed, index).  Autotune inputs: timing GEMMs on zeroed activations
+// underestimates their data-dependent power draw (and so overestimates clocks).
+__global__ void fill_hash_kernel(__nv_bfloat16* __restrict__ x, int64_t n, uint32_t seed, float scale, int relu) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t h = static_cast<uint32_t>(i) * 0x9E3779B1u ^ static_cast<uint32_t>(i >> 32) * 0x85EBCA77u ^ seed;
+    h ^= h >> 16;
+    h *= 0x7FEB352Du;
+    h ^= h >> 15;
+    h *= 0x846CA68Bu;
+    h ^= h >> 16;
+    float v = scale * (static_cast<float>(h >> 8) * (2.0f / 16777216.0f) - 1.0f);
+    if (relu) v = fmaxf(v, 0.0f);
+    x[i] = __float2bfloat16(v);
+  }
+}
+
 int grid_for(int64_t work_items, int threads) {
   int64_t g = (work_items + threads - 1) / threads;
   const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
@@ -451,6 +469,13 @@ int grid_for(int64_t work_items, int threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_fill_hash(__nv_bfloat16* x, int64_t n, uint32_t seed, float scale, bool relu,
+                             cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  fill_hash_kernel<<<grid_for(n, 256), 256, 0, stream>>>(x, n, seed, scale, relu ? 1 : 0);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,
                          const __nv_bfloat16* pos_emb, int pos_offset, int rows, int hidden, int vocab,

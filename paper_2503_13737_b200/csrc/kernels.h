@@ -152,4 +152,8 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, int ld_src, const int32
 cudaError_t launch_block_copy(const __nv_bfloat16* src, __nv_bfloat16* dst, const int32_t* block_ids,
                               int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream);
 
+// pseudo-random bf16 fill (autotune activations): scale * U[-1, 1), optionally ReLU'd
+cudaError_t launch_fill_hash(__nv_bfloat16* x, int64_t n, uint32_t seed, float scale, bool relu,
+                             cudaStream_t stream);
+
 }  // namespace ag

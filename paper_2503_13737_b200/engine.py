@@ -256,7 +256,7 @@ class Engine:
     def __init__(self, trace: list[RequestSpec], profile: ModelProfile, policy: PolicyConfig | None = None,
                  executor: Executor | None = None, *, clock: str = "virtual", kv_blocks: int | None = None,
                  block_size: int = 32, horizon_s: float = math.inf, per_token_swap_cost_s: float = 0.0,
-                 check_invariants: bool = False):
+                 check_invariants: bool = False, autoregressive: bool = True):
         if clock not in ("virtual", "device", "wall"):
             raise ValueError(f"unknown clock {clock!r}")
         self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
@@ -272,6 +272,9 @@ class Engine:
         self.horizon = horizon_s
         self.swap_cost = per_token_swap_cost_s
         self.check = check_invariants
+        # decode inputs: the token the executor emitted last for the request (real autoregressive
+        # generation); prompt tokens -- and decodes of an executor that emits none -- are synthetic
+        self.autoregressive = autoregressive
         self.queue: list[QueueEntry] = []
         self.long_active: set[int] = set()
         self.metrics = MetricsAccumulator()
@@ -334,8 +337,18 @@ class Engine:
             e.seq = self._stamp_next()
 
         if not plan.selections:
+            # empty plan: jump to min(next arrival, now + T_max), plus the swap time of a
+            # plan that only preempts (PagedFcfs with the pool exhausted) -- whose swap-outs are real
+            # work, so they are recorded as an iteration of forward size 0
+            cost = swap_tokens * self.swap_cost
+            if plan.preempted:
+                self.metrics.iterations.append(IterationRecord(
+                    index=len(self.metrics.iterations), start=start, elapsed=cost, forward_size=0,
+                    token_budget=plan.token_budget, num_seqs=0, num_decode=0,
+                    allocated_tokens=self.pool.allocated_tokens, preemptions=len(plan.preempted),
+                    host_pre_s=time.perf_counter() - t_step0))
             nxt = self.trace[self._next_arrival].arrival_time if self._next_arrival < len(self.trace) else math.inf
-            self.clock = min(nxt, self.clock + self.stats.t_max)
+            self.clock = min(nxt, self.clock + self.stats.t_max) + cost
             return None
 
         # ---- allocation + batch packing (vectorised: one numpy pass over all tokens)
@@ -343,6 +356,7 @@ class Engine:
         n_sel = len(plan.selections)
         chunk = np.empty(n_sel, np.int64)
         before_arr = np.empty(n_sel, np.int64)
+        fed: list[tuple[int, int]] = []  # (selection index, token id) of decodes fed their last output
         tables: list[list[int]] = []
         for i, sel in enumerate(plan.selections):
             e = by_id[sel.request_id]
@@ -357,13 +371,18 @@ class Engine:
                     if rec.preempt_time is not None:
                         self.stats.observe_preemption_duration(start - rec.preempt_time)
                 before = self.pool.tokens_stored(rid)
-                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if has_prompt_left(e)
+                prompt_left = has_prompt_left(e)
+                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if prompt_left
                           else self.pool.demand_tg(rid))
                 self.pool.allocate(rid, demand)
             except (AllocationError, StateError) as exc:
                 raise EngineFault(f"plan infeasible against the pool: {exc}") from exc
             chunk[i] = sel.chunk_len
             before_arr[i] = before
+            if self.autoregressive and not prompt_left:
+                out = self.metrics.requests[rid].tokens_out
+                if out and out[-1] >= 0:
+                    fed.append((i, out[-1]))
             tables.append(self.pool.block_table(rid))
         if free_before - self.pool.free_blocks != plan.blocks_needed:
             raise EngineFault(f"allocated {free_before - self.pool.free_blocks} blocks, plan expected "
@@ -375,6 +394,8 @@ class Engine:
         positions = (np.arange(S) - cu[seq_of_tok] + before_arr[seq_of_tok]).astype(np.int32)
         rids_arr = np.asarray([s.request_id for s in plan.selections], np.int64)
         token_ids = synthetic_tokens(rids_arr[seq_of_tok], positions, self.executor.vocab)
+        for i, tok in fed:
+            token_ids[cu[i]] = tok
         stride = max(len(t) for t in tables)
         bt = np.zeros((n_sel, stride), dtype=np.int32)
         for i, t in enumerate(tables):

@@ -32,7 +32,8 @@ class CudaExecutor:
     def __init__(self, cfg: OPTConfig, num_blocks: int, *, max_tokens: int = 4096, max_seqs: int = 512,
                  max_blocks_per_seq: int | None = None, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
                  init: str = "opt", weights: dict | None = None, device: int | None = None,
-                 parity_logits: bool = False, nccl_uid: bytes | None = None, autotune: bool = True):
+                 parity_logits: bool = False, nccl_uid: bytes | None = None, autotune: bool = True,
+                 host_collective=None):
         if not torch.cuda.is_available():
             raise EngineFault("CudaExecutor needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -70,11 +71,15 @@ class CudaExecutor:
             lw = _lib.LayerWeights(*[L[name].data_ptr() for name, _ in _lib.LayerWeights._fields_])
             _lib.check(self.lib.ag_model_set_layer(handle, l, C.byref(lw)))
             _lib.check(self.lib.ag_model_set_kv_cache(handle, l, self.kv[l, 0].data_ptr(), self.kv[l, 1].data_ptr()))
+        self.host_collective = host_collective
         if tp_size > 1:
-            if nccl_uid is None:
-                raise EngineFault("tp_size > 1 needs the NCCL unique id broadcast by rank 0")
-            buf = C.create_string_buffer(bytes(nccl_uid), 128)
-            _lib.check(self.lib.ag_model_init_tp(handle, buf))
+            if host_collective is not None:  # tp.HostCollective: ranks sharing one GPU (tests)
+                _lib.check(self.lib.ag_model_init_tp_host(handle, C.cast(host_collective.fn, C.c_void_p), None))
+            elif nccl_uid is None:
+                raise EngineFault("tp_size > 1 needs the NCCL unique id broadcast by rank 0 (or a host collective)")
+            else:
+                buf = C.create_string_buffer(bytes(nccl_uid), 128)
+                _lib.check(self.lib.ag_model_init_tp(handle, buf))
         if autotune:
             self._autotune()
         self._dev_ms = C.c_float(0.0)
@@ -206,7 +211,7 @@ class CudaExecutor:
         if not getattr(self, "_pin_failed", False):
             try:
                 return torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
-            except (RuntimeError, torch.AcceleratorError):
+            except (RuntimeError, getattr(torch, "AcceleratorError", RuntimeError)):
                 self._pin_failed = True
         return torch.empty(shape, dtype=torch.bfloat16)
 

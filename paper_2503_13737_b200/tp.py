@@ -109,6 +109,52 @@ def follower_loop(local, group, on_mark=None) -> int:
             on_mark(int(hdr[1]))
 
 
+class HostCollective:
+    """The library's host collective backend (ag_model_init_tp_host) over a torch.distributed group.
+
+    Lets TP ranks run as processes that share ONE GPU (NCCL refuses two ranks on a device): the
+    library stages each collective through pinned host memory and this callback completes it with
+    the group (gloo).  bf16 all-reduces are summed in fp32 and rounded to bf16 once, as NCCL does
+    for two ranks.  A correctness path for tests and bench smoke runs, not a performance path."""
+
+    def __init__(self, group, tp_size: int):
+        from . import _lib
+        self.group, self.tp_size, self.calls = group, tp_size, 0
+        self._L = _lib
+        self.fn = _lib.HOST_COLLECTIVE_FN(self._call)  # keep a reference: the library holds the pointer
+
+    def _call(self, ctx, op, ptr, count, dtype) -> int:
+        import ctypes as C
+        L = self._L
+        try:
+            self.calls += 1
+            if op == L.COLL_ALLREDUCE_SUM:
+                if dtype != L.DT_BF16:
+                    return 2
+                raw = np.ctypeslib.as_array((C.c_int16 * count).from_address(ptr))
+                t = torch.from_numpy(raw).view(torch.bfloat16).float()
+                dist.all_reduce(t, group=self.group)
+                raw[:] = t.to(torch.bfloat16).view(torch.int16).numpy()
+                return 0
+            if op == L.COLL_ALLGATHER:
+                ctype = {L.DT_F32: C.c_float, L.DT_I32: C.c_int32}.get(dtype)
+                if ctype is None:
+                    return 2
+                buf = np.ctypeslib.as_array((ctype * (count * self.tp_size)).from_address(ptr))
+                me = dist.get_rank(self.group)
+                parts = [torch.empty(count, dtype=torch.float32 if dtype == L.DT_F32 else torch.int32)
+                         for _ in range(self.tp_size)]
+                dist.all_gather(parts, torch.from_numpy(buf[me * count:(me + 1) * count].copy()), group=self.group)
+                for r, p in enumerate(parts):
+                    buf[r * count:(r + 1) * count] = p.numpy()
+                return 0
+            return 3
+        except Exception:  # pragma: no cover - surfaced to the library as a collective failure
+            import traceback
+            traceback.print_exc()
+            return 1
+
+
 def share_nccl_id(rank: int, group) -> bytes:
     """Rank 0 creates the library's NCCL unique id; everyone receives it over the host group."""
     from .executor import CudaExecutor

@@ -1,12 +1,16 @@
-"""End-to-end parity of the mixed-batch forward on the B200 vs the CPU oracle.
+"""End-to-end parity of the mixed-batch forward on the B200 vs the oracle.
 
 Tolerance (north_star): logits max-abs <= 2e-2 per step, greedy tokens identical for >= 99% of
-token events.  Scheduling is shared (TeeExecutor), so the device sees exactly the oracle's
-inputs (teacher-forced synthetic tokens, same block tables / slots)."""
+token events -- a disagreement is only excused where the oracle's own top-2 logit gap is within
+twice the tolerance (a near tie that bf16 rounding may legitimately flip).  Scheduling is shared
+(TeeExecutor), so the device sees exactly the oracle's inputs (teacher-forced synthetic tokens,
+same block tables / slots).  The full-depth OPT-13B and 100k-context cases run the oracle's torch
+restatement on the GPU in fp32 (TF32 off); the rest run it on the CPU."""
 import numpy as np
 import pytest
 import torch
 
+from batches import make_batch, split_prefill
 from oracle.executor import OracleExecutor, TeeExecutor
 from paper_2503_13737_b200 import configs, model as M, workload
 from paper_2503_13737_b200.engine import Engine
@@ -18,17 +22,38 @@ LOGIT_TOL = 2e-2
 TOKEN_AGREEMENT = 0.99
 
 
-def _compare(records):
-    worst, agree, total = 0.0, 0, 0
-    for batch, dev, ref in records:
-        n = len(batch.logit_rows)
+class Tally:
+    """Worst |dlogit| and greedy-token agreement over many logit rows."""
+
+    def __init__(self):
+        self.worst, self.agree, self.exempt, self.total = 0.0, 0, 0, 0
+
+    def add(self, dev_logits, dev_tokens, ref_logits, ref_tokens):
+        n = ref_logits.shape[0]
         if n == 0:
-            continue
-        d = (dev.logits[:n].float() - ref.logits[:n].float()).abs().max().item()
-        worst = max(worst, d)
-        agree += int((dev.token_ids[:n] == ref.token_ids[:n]).sum())
-        total += n
-    return worst, agree / max(total, 1), total
+            return
+        d = (dev_logits[:n].float() - ref_logits.float()).abs().max().item()
+        self.worst = max(self.worst, d)
+        same = torch.as_tensor(np.asarray(dev_tokens[:n]) == np.asarray(ref_tokens[:n]))
+        top2 = ref_logits.float().topk(2, dim=-1).values
+        tie = (top2[:, 0] - top2[:, 1]) <= 2 * LOGIT_TOL
+        self.agree += int(same.sum())
+        self.exempt += int(((~same) & tie).sum())
+        self.total += n
+
+    def check(self, label):
+        rate = self.agree / max(self.total, 1)
+        print(f"{label}: max|dlogit|={self.worst:.4g} tokens {self.agree}/{self.total} "
+              f"(agreement {rate:.4f}, near-tie exempt {self.exempt})")
+        assert self.worst <= LOGIT_TOL
+        assert rate >= TOKEN_AGREEMENT or self.agree + self.exempt == self.total
+
+
+def _compare(records):
+    t = Tally()
+    for batch, dev, ref in records:
+        t.add(dev.logits, dev.token_ids, ref.logits, ref.token_ids)
+    return t.worst, t.agree / max(t.total, 1), t.total
 
 
 def test_config1_trace_parity():
@@ -50,21 +75,7 @@ def test_config1_trace_parity():
     assert agree >= TOKEN_AGREEMENT
 
 
-def _make_batch(pool, cfg, segs):
-    from paper_2503_13737_b200.engine import DeviceBatch, synthetic_tokens
-    ids, pos, slot, cu, ctx, tabs, lrows, rids = [], [], [], [0], [], [], [], []
-    for rid, start, n in segs:
-        d = pool.demand_prompt_chunk(rid, n) if (n > 1 or not pool.is_resident(rid)) else pool.demand_tg(rid)
-        pool.allocate(rid, d)
-        p = np.arange(start, start + n, dtype=np.int32)
-        ids.append(synthetic_tokens(rid, p, cfg.vocab)); pos.append(p)
-        slot.append(np.asarray(pool.slots(rid, start, n), np.int32)); ctx.append(start)
-        cu.append(cu[-1] + n); tabs.append(pool.block_table(rid)); lrows.append(cu[-1] - 1); rids.append(rid)
-    bt = np.zeros((len(tabs), max(map(len, tabs))), np.int32)
-    for i, t in enumerate(tabs):
-        bt[i, :len(t)] = t
-    return DeviceBatch(rids, np.concatenate(ids), np.concatenate(pos), np.asarray(cu, np.int32),
-                       np.asarray(ctx, np.int32), bt, np.concatenate(slot), np.asarray(lrows, np.int32), rids)
+_make_batch = make_batch
 
 
 def test_13b_shape_mixed_batch_two_layers():
@@ -78,27 +89,44 @@ def test_13b_shape_mixed_batch_two_layers():
     dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=4096, max_seqs=128, weights=w, parity_logits=True)
     ref = OracleExecutor(cfg, w, pool.total_blocks)
     decodes = [(2 + i, 50 + 13 * i) for i in range(40)]
-    # prefixes, <= 4096 tokens per forward
-    prefill = [(0, 0, 3000)] + [(rid, 0, p) for rid, p in decodes]
-    batch, used = [], 0
-    for seg in prefill:
-        if used + seg[2] > 4000:
-            b = _make_batch(pool, cfg, batch)
-            dev.execute(b); ref.execute(b)
-            batch, used = [], 0
-        batch.append(seg)
-        used += seg[2]
-    b = _make_batch(pool, cfg, batch)
-    dev.execute(b); ref.execute(b)
-    mixed = [(0, 3000, 1500), (1, 0, 300)] + [(rid, p, 1) for rid, p in decodes]
-    b = _make_batch(pool, cfg, mixed)
+    tally = Tally()
+    for segs in split_prefill([(0, 0, 3000)] + [(rid, 0, p) for rid, p in decodes], 4000):
+        b = make_batch(pool, cfg, segs)
+        a, r = dev.execute(b), ref.execute(b)
+        tally.add(a.logits, a.token_ids, r.logits, r.token_ids)
+    b = make_batch(pool, cfg, [(0, 3000, 1500), (1, 0, 300)] + [(rid, p, 1) for rid, p in decodes])
     a, r = dev.execute(b), ref.execute(b)
-    n = len(b.logit_rows)
-    d = (a.logits[:n] - r.logits[:n]).abs().max().item()
-    agree = float((a.token_ids == r.token_ids).mean())
-    print(f"13B-shape mixed step: S_f={b.num_tokens} max|dlogit|={d:.4g} agreement={agree:.3f}")
-    assert d <= 5e-2
-    assert agree >= 0.95
+    tally.add(a.logits, a.token_ids, r.logits, r.token_ids)
+    tally.check(f"13B-shape 2 layers, mixed S_f={b.num_tokens}")
+
+
+def test_opt13b_full_depth_mixed_steps_vs_oracle():
+    """The named architecture at full depth: all 40 OPT-13B layers (config-2 shape, random biases and
+    LayerNorm affine so every epilogue term is live), autotuned GEMM plans as in production.  After
+    prefilling a 3k-token prompt and 48 short prompts, three mixed steps: a 1024-token chunk on the 3k
+    prefix + a fresh 500-token prompt + 48 decodes; then decodes + a new 200-token prompt; then decodes
+    + that prompt's first decode + a 37-token prompt.  Oracle: the same restatement in fp32 on the GPU."""
+    from paper_2503_13737_b200.executor import CudaExecutor
+    from paper_2503_13737_b200.kvc import BlockPool
+    cfg = M.opt_13b(max_positions=8192)
+    w = M.init_weights(cfg, seed=13, device="cuda", init="test")
+    pool = BlockPool(512)
+    dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=4096, max_seqs=64, weights=w, parity_logits=True)
+    ref = OracleExecutor(cfg, w, pool.total_blocks, device="cuda")
+    dec = [(2 + i, 16 + 5 * i) for i in range(48)]
+    plan = split_prefill([(0, 0, 3000)] + [(rid, 0, p) for rid, p in dec], 4096)
+    plan += [
+        [(0, 3000, 1024), (1, 0, 500)] + [(rid, p, 1) for rid, p in dec],
+        [(0, 4024, 1), (1, 500, 1), (60, 0, 200)] + [(rid, p + 1, 1) for rid, p in dec],
+        [(0, 4025, 1), (1, 501, 1), (60, 200, 1), (61, 0, 37)] + [(rid, p + 2, 1) for rid, p in dec],
+    ]
+    tally = Tally()
+    for segs in plan:
+        b = make_batch(pool, cfg, segs)
+        a, r = dev.execute(b), ref.execute(b)
+        tally.add(a.logits, a.token_ids, r.logits, r.token_ids)
+    tally.check("OPT-13B 40 layers, 6 forwards")
+    assert tally.total >= 150
 
 
 def _prompt_batch(pool, cfg, rid, tok_rid, start, n):
@@ -114,12 +142,13 @@ def _prompt_batch(pool, cfg, rid, tok_rid, start, n):
                        np.asarray([n - 1], np.int32), [rid])
 
 
-def test_long_context_100k_chunk_invariance():
+def test_long_context_100k_vs_oracle_and_chunk_invariance():
     """Config-4 regime on one GPU (2 OPT-13B-shaped layers): a 100k-token prompt prefilled in
-    16384-token chunks and, as a second request with the same tokens, in 12000-token chunks, then
-    one decode each.  Chunked prefill must not change the result (SURVEY §7 property): last-chunk
-    and decode logits agree within the bf16 tolerance and pick the same greedy token.  Exercises
-    split-KV tile attention over ~3k-page block tables and the extended position table."""
+    16384-token chunks -- every chunk checked against the oracle (fp32 on the GPU) -- then one decode;
+    and, as a second request with the same tokens, in 12000-token chunks.  Chunked prefill must not
+    change the result (SURVEY §7 property): last-chunk and decode logits agree within the bf16
+    tolerance and pick the same greedy token.  Exercises split-KV tile attention over ~3k-page block
+    tables, decode rows over a 100k context and the extended position table."""
     import os
     from paper_2503_13737_b200.executor import CudaExecutor
     from paper_2503_13737_b200.kvc import BlockPool
@@ -133,18 +162,29 @@ def test_long_context_100k_chunk_invariance():
         dev = CudaExecutor(cfg, pool.total_blocks, max_tokens=16384, max_seqs=8, weights=w, parity_logits=True)
     finally:
         os.environ.pop("AG_DETERMINISTIC", None)
+    ref = OracleExecutor(cfg, w, pool.total_blocks, device="cuda")
+    tally = Tally()
     outs = []
     for rid, chunk in ((0, 16384), (1, 12000)):
         res = None
         for start in range(0, P, chunk):
-            res = dev.execute(_prompt_batch(pool, cfg, rid, 0, start, min(chunk, P - start)))
-        dec = dev.execute(_prompt_batch(pool, cfg, rid, 0, P, 1))
+            b = _prompt_batch(pool, cfg, rid, 0, start, min(chunk, P - start))
+            res = dev.execute(b)
+            if rid == 0:
+                r = ref.execute(b)
+                tally.add(res.logits, res.token_ids, r.logits, r.token_ids)
+        b = _prompt_batch(pool, cfg, rid, 0, P, 1)
+        dec = dev.execute(b)
+        if rid == 0:
+            r = ref.execute(b)
+            tally.add(dec.logits, dec.token_ids, r.logits, r.token_ids)
         outs.append((res.logits[:1].float().clone(), res.token_ids.copy(), dec.logits[:1].float().clone(),
                      dec.token_ids.copy()))
+    tally.check("100k prompt (16384-token chunks + 1 decode) vs oracle")
     (la, ta, da, tda), (lb, tb, db, tdb) = outs
     d_last = (la - lb).abs().max().item()
     d_dec = (da - db).abs().max().item()
-    print(f"100k prompt: max|dlogit| last-chunk {d_last:.4g}, decode {d_dec:.4g}")
+    print(f"100k prompt chunk invariance: max|dlogit| last-chunk {d_last:.4g}, decode {d_dec:.4g}")
     assert torch.isfinite(la).all() and torch.isfinite(da).all()
     # the two chunkings give the GEMMs different M, hence possibly different tile / split-K plans and
     # fp32 summation orders: equal within the bf16 tolerance (bitwise only when the plans coincide)
@@ -186,7 +226,7 @@ def test_split_k_atomic_epilogue_forward(bn, splits, am):
         worst = max(worst, (a.logits[:n] - r.logits[:n]).abs().max().item())
         assert np.array_equal(a.token_ids[:n], r.token_ids[:n])
     print(f"plan {bn_}x{splits}a{am_}: max|dlogit|={worst:.4g}")
-    assert worst <= 5e-2
+    assert worst <= LOGIT_TOL
 
 
 def test_175b_shape_two_layers_vs_oracle():

@@ -182,6 +182,18 @@ def _attn_case(seqs, heads, seed):
     return q, kp, vp, bt, cu, ctx
 
 
+ATTN_REL_TOL = 2e-2
+
+
+def _attn_err(out, ref, heads):
+    """Max over (query row, head) of max|out - ref| / max|ref| within that row-head's 128 dims.
+    Normalised per row-head so long contexts -- whose outputs average ~N(0,1) values over up to
+    100k keys and are ~1e-2 in magnitude -- cannot pass with a grossly wrong result."""
+    d = (out.float().cpu() - ref.cpu()).abs().reshape(-1, heads, 128).amax(-1)
+    scale = ref.cpu().abs().reshape(-1, heads, 128).amax(-1).clamp_min(1e-6)
+    return (d / scale).max().item()
+
+
 @pytest.mark.parametrize("seqs,heads", [
     ([(0, 100)], 2),
     ([(37, 1), (0, 5), (1000, 1), (0, 64), (5, 17)], 3),
@@ -195,8 +207,8 @@ def test_mixed_attention(K, seqs, heads):
     out = K.paged_attention(q.to(DEV), kp.to(DEV), vp.to(DEV), bt.to(DEV), cu, ctx)
     torch.cuda.synchronize()
     ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
-    err = (out.float().cpu() - ref).abs().max().item()
-    assert err <= 2e-2, err
+    err = _attn_err(out, ref, heads)
+    assert err <= ATTN_REL_TOL, err
 
 
 @pytest.mark.parametrize("seqs,heads", [
@@ -217,21 +229,21 @@ def test_mixed_attention_boundaries(K, seqs, heads):
     out = K.paged_attention(q.to(DEV), kp.to(DEV), vp.to(DEV), bt.to(DEV), cu, ctx)
     torch.cuda.synchronize()
     ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
-    err = (out.float().cpu() - ref).abs().max().item()
-    assert err <= 2e-2, err
+    err = _attn_err(out, ref, heads)
+    assert err <= ATTN_REL_TOL, err
 
 
 def test_mixed_attention_back_to_back(K):
-    """Persistent tile CTAs take units from a device counter that the last CTA of each launch
-    resets: consecutive launches of different shapes must each cover all their units."""
+    """Consecutive launches of different shapes reuse the same host-built work-list buffers and
+    split-KV partial workspace: each launch must cover exactly its own units (no stale items)."""
     cases = [([(0, 700)] * 3, 40), ([(2000, 129), (0, 5)], 40), ([(0, 700)] * 3, 40)]
     for seqs, heads in cases:
         q, kp, vp, bt, cu, ctx = _attn_case(seqs, heads, seed=11)
         out = K.paged_attention(q.to(DEV), kp.to(DEV), vp.to(DEV), bt.to(DEV), cu, ctx)
         torch.cuda.synchronize()
         ref = orc.paged_attention(q.float(), kp, vp, bt, cu, ctx)
-        err = (out.float().cpu() - ref).abs().max().item()
-        assert err <= 2e-2, (seqs[:2], err)
+        err = _attn_err(out, ref, heads)
+        assert err <= ATTN_REL_TOL, (seqs[:2], err)
 
 
 def test_kv_swap_roundtrip(K):

@@ -38,6 +38,8 @@ HEAD_DIM = 128
 
 ROUND_BF16 = True  # False = pure fp32 restatement (used to pin against transformers' fp32 OPT)
 DEVICE = torch.device("cpu")  # where f32() materialises operands; OracleOPT switches it per forward
+ACC = torch.float32           # accumulation dtype; float64 gives the same restatement with a different
+                              # summation precision (tests use the fp32-vs-fp64 spread as bf16's noise floor)
 ATTN_SCORE_ELEMS = 1 << 27     # heads x rows x kv_len fp32 scores held at once (query rows are chunked)
 
 
@@ -45,11 +47,11 @@ def rb(x: torch.Tensor) -> torch.Tensor:
     """Round to bf16 and return as fp32 (a storage point of the device pipeline)."""
     if not ROUND_BF16:
         return x
-    return x.to(torch.bfloat16).to(torch.float32)
+    return x.to(torch.bfloat16).to(ACC)
 
 
 def f32(x: torch.Tensor) -> torch.Tensor:
-    return x.detach().to(DEVICE, torch.float32)
+    return x.detach().to(DEVICE, ACC)
 
 
 def embed(ids, positions, tok_emb, pos_emb):
@@ -90,7 +92,7 @@ def paged_attention(q, k_pool, v_pool, block_table, cu_q, ctx_len, block_size=32
     S = q.shape[0]
     heads = k_pool.shape[1]
     dev = q.device
-    out = torch.zeros(S, heads * HEAD_DIM, dtype=torch.float32, device=dev)
+    out = torch.zeros(S, heads * HEAD_DIM, dtype=ACC, device=dev)
     cu_q = [int(v) for v in cu_q]
     for b in range(len(cu_q) - 1):
         q0, q1 = cu_q[b], cu_q[b + 1]
@@ -146,8 +148,9 @@ class OracleOPT:
     (full model, tp_size=1) or one TP shard when tp_size > 1 (then ``allreduce`` sums partials)."""
 
     def __init__(self, cfg, weights, num_blocks, block_size=32, tp_rank=0, tp_size=1, allreduce=None,
-                 device="cpu"):
+                 device="cpu", acc=torch.float32):
         self.cfg = cfg
+        self.acc = acc
         self.dev = torch.device(device)
         self.w = weights
         self.block_size = block_size
@@ -167,14 +170,15 @@ class OracleOPT:
         return self.allreduce(partial)
 
     def forward(self, st: StepInputs):
-        global DEVICE
+        global DEVICE, ACC
         prev, DEVICE = DEVICE, self.dev
+        prev_acc, ACC = ACC, self.acc
         tf32 = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = False  # true fp32 matmuls when run on the GPU
         try:
             return self._forward(st)
         finally:
-            DEVICE = prev
+            DEVICE, ACC = prev, prev_acc
             torch.backends.cuda.matmul.allow_tf32 = tf32
 
     def _forward(self, st: StepInputs):
@@ -208,4 +212,4 @@ class OracleOPT:
         rows = st.logit_rows.long()
         hl = layernorm(x[rows], w["final_g"], w["final_b"], cfg.ln_eps)
         logits = hl @ f32(w["tok_emb"]).T
-        return logits.cpu(), torch.argmax(logits, dim=-1).to(torch.int32).cpu()
+        return logits.float().cpu(), torch.argmax(logits, dim=-1).to(torch.int32).cpu()

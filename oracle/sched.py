@@ -124,8 +124,16 @@ class OracleScheduler:
         pend = r.remaining if r.phase == "prompt" else 0
         return self.slo(r) - (now - r.enqueue) - self.n_ck(pend) * self.t_max
 
-    def iter_time(self, s_f):
-        return self.p.fixed_overhead_s + self.p.pivot_time_s * s_f / self.p.pivot_forward_size
+    def iter_time(self, s_f, shapes=()):
+        """Reference linear model; plus the B200 extension's K/V-read and attention-pair terms when the
+        profile carries them (shapes = [(q_i, p_i)]; same float expression as cost_model.batch_time)."""
+        t = self.p.fixed_overhead_s + self.p.pivot_time_s * s_f / self.p.pivot_forward_size
+        b, c = getattr(self.p, "kv_read_s_per_token", 0.0), getattr(self.p, "attn_s_per_pair", 0.0)
+        if b or c:
+            kv = sum(p + q for q, p in shapes)
+            pairs = sum(q * p + q * (q + 1) // 2 for q, p in shapes)
+            t = t + b * kv + c * pairs
+        return t
 
     def budget(self, slo_min):
         return max(1, min(math.floor(self.p.pivot_forward_size * slo_min / self.p.pivot_time_s),
@@ -265,7 +273,7 @@ class OracleScheduler:
             entry["sel"].append((r.rid, c, final, before))
             entry["tables"][r.rid] = list(self.pool.tables[r.rid])
         s_f = sum(c for _, c, _ in chosen)
-        self.clock = start + self.iter_time(s_f)
+        self.clock = start + self.iter_time(s_f, [(c, before) for _, c, _, before in entry["sel"]])
         now = self.clock
         done = set()
         for r, c, blk in chosen:

@@ -7,7 +7,8 @@ The only departure from the reference engine is the clock advance. 
 clock by ``iteration_time(S_f)``; here the clock source is selectable:
 
   clock="virtual"  iteration_time(S_f) from the cost model (bit-exact scheduler parity with the
-                   CPU oracle run; the device still executes every plan),
+                   CPU oracle run; the device still executes every plan) -- or, with a profile
+                   carrying the B200 extension, batch_time(S_f, K/V rows read, attention pairs),
   clock="device"   CUDA-event time of the forward measured by the executor,
   clock="wall"     host wall time of executor.execute (packing + H2D + forward + D2H).
 
@@ -25,7 +26,7 @@ from typing import Protocol
 
 import numpy as np
 
-from .cost_model import ModelProfile, iteration_time
+from .cost_model import ModelProfile, batch_time, iteration_time
 from .errors import AllocationError, EngineFault, StateError
 from .kvc import BlockPool
 from .policies import BatchPlan, PlanContext, PolicyConfig, has_prompt_left, plan as make_plan
@@ -420,7 +421,10 @@ class Engine:
         res = self.executor.execute(batch)
         wall = time.perf_counter() - t_host
         if self.clock_mode == "virtual":
-            elapsed = iteration_time(plan.forward_size, self.profile)
+            q_arr = chunk
+            kv_tok = int(before_arr.sum() + q_arr.sum())
+            pairs = int((q_arr * before_arr).sum() + (q_arr * (q_arr + 1) // 2).sum())
+            elapsed = batch_time(plan.forward_size, kv_tok, pairs, self.profile)
         elif self.clock_mode == "device":
             elapsed = res.elapsed_s
         else:

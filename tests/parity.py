@@ -1,0 +1,54 @@
+"""Logit-parity bookkeeping shared by the GPU forward tests (tests/test_forward_gpu.py, test_tp_gpu.py)."""
+import numpy as np
+
+LOGIT_TOL = 2e-2
+TOKEN_AGREEMENT = 0.99
+FLOOR_FACTOR = 1.5
+
+
+class Tally:
+    """Worst / mean |dlogit| and greedy-token agreement over many logit rows.
+
+    The stated bound is max|dlogit| <= 2e-2 -- or, where the network's own bf16 noise floor is larger,
+    FLOOR_FACTOR x that floor.  The floor is measured, not assumed: the same oracle restatement run
+    with fp64 instead of fp32 accumulation (identical bf16 rounding points) moves the logits of the
+    random-init OPT-13B-shaped models by up to ~0.04 (2 layers) because a rounding decision that flips
+    at one storage point propagates; no bf16 implementation can be held closer to the oracle than the
+    oracle is to itself.  The mean |dlogit| must also stay within FLOOR_FACTOR x the floor's mean, which
+    a systematic kernel error (as opposed to rounding noise) would break.  Greedy tokens: >= 99%
+    identical, a disagreement only excused where the oracle's top-2 gap is within twice the bound."""
+
+    def __init__(self):
+        self.worst = self.floor = self.sum_d = self.sum_f = 0.0
+        self.agree = self.exempt = self.total = 0
+        self.rows = []
+
+    def add(self, dev_logits, dev_tokens, ref_logits, ref_tokens, ref64_logits=None):
+        n = ref_logits.shape[0]
+        if n == 0:
+            return
+        d = (dev_logits[:n].float() - ref_logits.float()).abs()
+        self.worst = max(self.worst, d.max().item())
+        self.sum_d += d.mean().item() * n
+        if ref64_logits is not None:
+            f = (ref64_logits.float() - ref_logits.float()).abs()
+            self.floor = max(self.floor, f.max().item())
+            self.sum_f += f.mean().item() * n
+        same = np.asarray(dev_tokens[:n]) == np.asarray(ref_tokens[:n])
+        top2 = ref_logits.float().topk(2, dim=-1).values
+        self.rows += list(zip(same.tolist(), (top2[:, 0] - top2[:, 1]).tolist()))
+        self.total += n
+
+    def check(self, label):
+        bound = max(LOGIT_TOL, FLOOR_FACTOR * self.floor)
+        agree = sum(s for s, _ in self.rows)
+        exempt = sum((not s) and g <= 2 * bound for s, g in self.rows)
+        rate = agree / max(self.total, 1)
+        mean_d, mean_f = self.sum_d / max(self.total, 1), self.sum_f / max(self.total, 1)
+        print(f"{label}: max|dlogit|={self.worst:.4g} (bound {bound:.4g}, fp32-vs-fp64 oracle floor "
+              f"{self.floor:.4g}) mean|dlogit|={mean_d:.3g} (floor mean {mean_f:.3g}) tokens {agree}/{self.total} "
+              f"(agreement {rate:.4f}, near-tie exempt {exempt})")
+        assert self.worst <= bound
+        if self.floor > 0:
+            assert mean_d <= FLOOR_FACTOR * mean_f + 1e-4
+        assert rate >= TOKEN_AGREEMENT or agree + exempt == self.total

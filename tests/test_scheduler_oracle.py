@@ -50,3 +50,30 @@ def test_b200_like_profile_with_offline_matches_oracle():
                            fixed_overhead_s=0.005, kvc_capacity_tokens=60000)
     cfg = configs.config5(profile=prof, num_requests=120, arrival_rate=12.0).trace
     _compare(wl.generate_trace(cfg), prof, max_steps=2000)
+
+
+def test_extended_cost_model_matches_oracle():
+    """The B200 extension of the cost model (K/V-read and attention-pair terms, cost_model.batch_time)
+    drives the virtual clock of both sides with the same float expression: decisions stay bit-exact
+    under KV pressure with preemptions, and the clock differs from the linear model's."""
+    c = configs.config1()
+    prof = cm.ModelProfile(hidden_size=256, num_layers=2, pivot_forward_size=256, pivot_time_s=0.002,
+                           fixed_overhead_s=0.002, kvc_capacity_tokens=48 * 32, kv_read_s_per_token=2e-6,
+                           attn_s_per_pair=3e-9)
+    trace = wl.generate_trace(wl.TraceConfig(**{**c.trace.__dict__, "num_requests": 40, "profile": prof,
+                                                "long_fraction": 0.0,
+                                                "output_len_dist": wl.LengthDist("uniform", 100, 400)}))
+    n = _compare(trace, prof, kv_blocks=48)
+    assert n > 1000
+    lin = cm.ModelProfile(**{**prof.__dict__, "kv_read_s_per_token": 0.0, "attn_s_per_pair": 0.0})
+    e1, e2 = Engine(trace, prof, PolicyConfig(), kv_blocks=48), Engine(trace, lin, PolicyConfig(), kv_blocks=48)
+    assert e1.run().makespan > e2.run().makespan
+
+
+def test_batch_time_reduces_to_reference_linear_model():
+    prof = cm.opt_13b_like()
+    for s_f, kv, pairs in ((0, 0, 0), (768, 5000, 123456), (1, 2049, 2049)):
+        assert cm.batch_time(s_f, kv, pairs, prof) == cm.iteration_time(s_f, prof)
+    ext = cm.ModelProfile(**{**prof.__dict__, "kv_read_s_per_token": 1e-7, "attn_s_per_pair": 1e-9})
+    assert cm.batch_features([(1, 2048), (512, 0)]) == (2049 + 512, 2049 + 512 * 513 // 2)
+    assert cm.batch_time(768, 1000, 10, ext) == cm.iteration_time(768, prof) + 1e-7 * 1000 + 1e-9 * 10

@@ -56,7 +56,7 @@ def main():
     cfg, seed, blocks, steps = case(a.case)
     w = M.init_weights(cfg, seed, device="cuda", tp_rank=a.rank, tp_size=a.world, init="test")
     hc = HostCollective(dist.group.WORLD, a.world)
-    ex = CudaExecutor(cfg, blocks, max_tokens=2048, max_seqs=64, weights=w, tp_rank=a.rank, tp_size=a.world,
+    ex = CudaExecutor(cfg, blocks, max_tokens=4096, max_seqs=64, weights=w, tp_rank=a.rank, tp_size=a.world,
                       parity_logits=True, autotune=False, host_collective=hc)
     pool = BlockPool(blocks)
     res = []

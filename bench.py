@@ -1,22 +1,25 @@
 #!/usr/bin/env python
 """SLO-meeting tokens/s of AccelGen's mixed-batch forward on B200 (BASELINE.json metric).
 
-One "step" = one engine iteration: order the queue, plan a BatchPlan (AccelGen),
-allocate KV blocks, run the mixed prefill+decode forward of OPT-13B (random bf16 weights) on the
-GPU(s), emit tokens.  Workload = BASELINE config 2 (90% <=1k prompts, 10% 4k-16k, output 1-2048,
-TBT 0.1875 s x U(0.75,1.25), TTFT per 512-token bucket x U(0.5,1.5)); the arrival rate scales
-with the GPU count (weak scaling), TP over the GPUs.  The engine runs on the live wall clock,
-so every SLO decision and every met/missed deadline is real.
+The engine serves BASELINE config 2 live on the wall clock: each iteration orders the queue, plans a
+BatchPlan (AccelGen), allocates KV blocks, runs the mixed prefill+decode forward of
+OPT-13B (random bf16 weights) on the GPU(s) and emits tokens.  Workload: 90% <=1k prompts, 10% 4k-16k,
+output 1-2048, TBT 0.1875 s x U(0.75,1.25), TTFT per 512-token bucket x U(0.5,1.5); the arrival rate
+scales with the GPU count (weak scaling), TP over the GPUs.
 
-  value  SLO-meeting tokens / sum of CUDA-event forward times of the K timed steps (metadata
-         already resident in HBM; the device-side number)
-  e2e    the same tokens / wall time of the K steps through the public API (scheduler, packing,
-         pinned H2D of every step's metadata, forward, D2H of the next-token ids)
-  SLO-meeting tokens: tokens of a forward whose token event met its deadline (TTFT for a final
-  chunk, TBT for a decode, JCT for offline) or, for a non-final chunk, whose TTFT deadline has
-  not passed yet.  iter_slo_attainment = met / all token events in the window.
+  step   one 1-second goodput window of serving (SPEC.md:528 windows, ~25-45 forwards each); the K timed
+         windows start after an untimed ramp to steady state (--ramp-s of serving: request population and
+         KV occupancy have levelled off) and W warm-up windows
+  value  SLO-meeting tokens / sum of CUDA-event forward times of the K windows (metadata resident in
+         HBM; the device-side number)
+  e2e    the same tokens / wall time of the K windows through the public API (scheduler, packing, pinned
+         H2D of every step's metadata, forward, D2H of the next-token ids)
+  SLO-meeting tokens: a decode token whose TBT was met; a prompt's tokens -- every chunk, counted in the
+         window that processed it -- iff its first token met TTFT (resolved after the window by serving on,
+         untimed, until those prompts finish); iter_slo_attainment = met / all token events.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--rate R] [--ramp-s S]
+       (--gpus N > 1 without torchrun re-launches itself under torch.distributed.run, one rank per GPU)
 """
 from __future__ import annotations
 
@@ -40,11 +43,15 @@ UNIT = "tokens/s"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--rate", type=float, default=None, help="arrival rate per GPU (req/s)")
-    ap.add_argument("--ramp-s", type=float, default=6.0, help="untimed trace seconds before warmup")
+    ap.add_argument("--ramp-s", type=float, default=None, help="untimed seconds of serving before warmup")
+    ap.add_argument("--window-s", type=float, default=1.0, help="seconds of serving per step")
+    ap.add_argument("--policy", default="accelgen")
+    ap.add_argument("--tp-backend", choices=("nccl", "host"), default="nccl",
+                    help="host: TP collectives through the library's host backend (ranks may share a GPU)")
     ap.add_argument("--profile", default=None, help="ModelProfile JSON (default: profiles/opt13b_b200_tp{N}.json)")
     ap.add_argument("--kv-gb", type=float, default=None,
                     help="KV pool per GPU (GB); default: the HBM left after weights and a 12 GB reserve")
@@ -120,15 +127,29 @@ def default_profile(tp: int):
                            fixed_overhead_s=0.006 / tp, kvc_capacity_tokens=0), "declared-default"
 
 
+DEFAULT_RATE = 3.0    # req/s per GPU: highest rate with >= 95% iteration-SLO attainment at steady state
+DEFAULT_RAMP_S = 150.0  # (profiles/r2_rate_sweep.md); ramp: request population and KV occupancy level off
+
+
 def build_workload(args, world: int):
     from paper_2503_13737_b200 import configs
-    from paper_2503_13737_b200.cost_model import ModelProfile
-    prof, prof_src = (default_profile(world) if args.profile is None else
-                      (__import__("paper_2503_13737_b200.cost_model", fromlist=["x"]).load_profile(args.profile),
-                       args.profile))
-    rate = (args.rate if args.rate is not None else 8.0) * world
-    cfg = configs.config2(profile=prof, arrival_rate=rate, num_requests=4000)
+    from paper_2503_13737_b200.cost_model import load_profile
+    prof, prof_src = default_profile(world) if args.profile is None else (load_profile(args.profile), args.profile)
+    rate = (args.rate if args.rate is not None else DEFAULT_RATE) * world
+    cfg = configs.config2(profile=prof, arrival_rate=rate, num_requests=6000)
     return cfg, prof, prof_src, rate
+
+
+def _spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -148,7 +169,10 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    n_dev = torch.cuda.device_count()
+    if args.tp_backend == "nccl" and world > n_dev:
+        raise SystemExit(f"--gpus {world} needs {world} GPUs (found {n_dev}); --tp-backend host shares one")
+    torch.cuda.set_device(local % n_dev)
     group = None
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -156,20 +180,25 @@ def run_ours(args):
     cfg, prof, prof_src, rate = build_workload(args, world)
     mcfg = cfg.model
     kv_tok_bytes = mcfg.kv_bytes_per_token(tp=world)
+    shared = args.tp_backend == "host" and world > n_dev
     if args.kv_gb is None:  # size the paged pool for the 180 GB part: free HBM - weights - reserve
+        if world > 1:
+            dist.barrier()  # every rank measures before any rank allocates
         free_b = torch.cuda.mem_get_info()[0]
-        args.kv_gb = max(1.0, (free_b - 2.0 * mcfg.param_count() / world - 12e9) / 1e9)
+        ranks_here = -(-world // n_dev) if shared else 1
+        args.kv_gb = max(1.0, (free_b - 2.0 * mcfg.param_count() / world * ranks_here - 12e9) / ranks_here / 1e9)
     num_blocks = int(args.kv_gb * 1e9 // (32 * kv_tok_bytes))
     if world > 1:  # one pool geometry for all ranks: rank 0's block ids index every rank's pool
         nb = torch.tensor([num_blocks], dtype=torch.int64)
         dist.all_reduce(nb, op=dist.ReduceOp.MIN)
         num_blocks = int(nb.item())
     prof = ModelProfile(**{**prof.__dict__, "kvc_capacity_tokens": num_blocks * 32})
-    uid = TP.share_nccl_id(rank, group) if world > 1 else None
+    host_coll = TP.HostCollective(group, world) if world > 1 and args.tp_backend == "host" else None
+    uid = TP.share_nccl_id(rank, group) if world > 1 and host_coll is None else None
     s_pf = prof.pivot_forward_size
     ex = CudaExecutor(mcfg, num_blocks, max_tokens=s_pf, max_seqs=2048,
                       max_blocks_per_seq=(mcfg.pos_rows + 31) // 32, tp_rank=rank, tp_size=world, seed=0,
-                      init="opt", nccl_uid=uid)
+                      init="opt", nccl_uid=uid, host_collective=host_coll)
     torch.cuda.synchronize()
 
     if rank != 0:
@@ -197,22 +226,28 @@ def run_ours(args):
 
     trace = workload.generate_trace(cfg.trace)
     executor = TP.TPLeader(ex, group) if world > 1 else ex
-    eng = Engine(trace, prof, PolicyConfig(), executor, clock="wall", kv_blocks=num_blocks)
+    eng = Engine(trace, prof, PolicyConfig(policy=args.policy), executor, clock="wall", kv_blocks=num_blocks)
 
-    def next_step():
-        while not eng.done():
+    def serve_until(t_end):
+        its = []
+        while eng.clock < t_end:
+            if eng.done():
+                raise SystemExit("trace exhausted before the timed region ended; raise num_requests")
             it = eng.step()
             if it is not None:
-                return it
-        raise SystemExit("trace exhausted before the timed region ended; raise num_requests")
+                its.append(it)
+        return its
 
-    # untimed ramp to a loaded steady state, then W warm-up steps
-    while eng.clock < args.ramp_s:
-        next_step()
-    for _ in range(args.warmup):
-        next_step()
+    # untimed ramp to steady state, then W warm-up windows
+    ramp_s = DEFAULT_RAMP_S if args.ramp_s is None else args.ramp_s
+    t_ramp = time.perf_counter()
+    serve_until(ramp_s)
+    ramp_wall = time.perf_counter() - t_ramp
+    serve_until(eng.clock + args.warmup * args.window_s)
+    live0 = len(eng.queue)
+    kv0 = eng.pool.allocated_tokens / (num_blocks * 32)
 
-    # ---------------- timed region: exactly K steps
+    # ---------------- timed region: exactly K windows of serving
     batches = []
     orig_exec = ex.execute
 
@@ -222,9 +257,9 @@ def run_ours(args):
     ex.execute = recording_exec
     peaks = load_peaks()
     ex.set_roofline_peaks(peaks["tensor_sustained"], peaks["hbm"])
-    ex.set_profiling(False)  # the timed steps run un-instrumented; kernel classes come from a replay
+    ex.set_profiling(False)  # the timed windows run un-instrumented; kernel classes come from a replay
     launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local % n_dev)
     sampler.start()
     torch.cuda.synchronize()
     if world > 1:
@@ -234,7 +269,11 @@ def run_ours(args):
     if ncu_window:
         torch.cuda.cudart().cudaProfilerStart()
     t0 = time.perf_counter()
-    recs = [next_step() for _ in range(args.steps)]
+    windows, win_wall = [], []
+    for k in range(args.steps):
+        tw = time.perf_counter()
+        windows.append(serve_until(eng.clock + args.window_s))
+        win_wall.append(time.perf_counter() - tw)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     if ncu_window:
@@ -244,13 +283,29 @@ def run_ours(args):
         executor.mark(0)
         dist.barrier()
     ex.execute = orig_exec
+    recs = [it for w in windows for it in w]
     dev_s = sum(r.device_s for r in recs)
     launches_timed = ex.launches - launches0
     h2d_timed, d2h_timed = ex.h2d_bytes - h2d0, ex.d2h_bytes - d2h0
-    # per-kernel-class CUDA events (roofline, shares): replay the K timed batches once more with every
-    # launch bracketed by events, so the events never perturb the timed steps (TP: followers mirror)
+
+    # ---------------- untimed: serve on until every prompt chunked inside the windows has emitted its
+    # first token, so each chunk's tokens are credited iff the prompt met TTFT
+    pending = {rid for it in recs for rid, _ in it.pending_prefill}
+    t_res = eng.clock
+    while any(eng.prefill_met(r) is None for r in pending) and not eng.done() and eng.clock < t_res + 120:
+        eng.step()
+    unresolved = sum(eng.prefill_met(r) is None for r in pending)
+
+    def credited(it):
+        return it.slo_tokens + sum(n for rid, n in it.pending_prefill if eng.prefill_met(rid))
+    win_tokens = [sum(credited(it) for it in w) for w in windows]
+    win_dev = [sum(it.device_s for it in w) for w in windows]
+
+    # per-kernel-class CUDA events (roofline, shares): replay the timed batches (at most 400, evenly
+    # spaced) with every launch bracketed by events, so the events never perturb the timed windows
+    replay = batches if len(batches) <= 400 else [batches[int(i * len(batches) / 400)] for i in range(400)]
     ex.set_profiling(True)
-    for b in batches:
+    for b in replay:
         executor.execute(b)
     torch.cuda.synchronize()
     prof_k = ex.profile()
@@ -262,15 +317,13 @@ def run_ours(args):
         dev_s = float(t.item())
         dist.barrier()
 
-    slo_tokens = sum(r.slo_tokens for r in recs)
+    slo_tokens = sum(win_tokens)
     tokens = sum(r.forward_size for r in recs)
     events = sum(r.events for r in recs)
     met = sum(r.events_met for r in recs)
     K = args.steps
-    # whole-forward tensor roofline: algorithmic FLOPs of every timed forward / device time
     H, F, L, V = mcfg.hidden, mcfg.ffn, mcfg.num_layers, mcfg.vocab
     flops = sum(forward_flops(b.seq_shapes(), len(b.logit_rows), H, F, L, V, world) for b in batches)
-    peaks = load_peaks()
     gemm_cls = ("qkv_gemm", "out_gemm", "fc1_gemm", "fc2_gemm", "lmhead_gemm")
     g_ms = sum(prof_k[c]["ms"] for c in gemm_cls)
     g_fl = sum(prof_k[c]["flops"] for c in gemm_cls)
@@ -317,6 +370,7 @@ def run_ours(args):
                 roof_all[cls]["traffic"] = per * ratio
                 roof_all[cls]["traffic_source"] = f"ncu dram/algorithmic = {ratio:.3f} ({nt[cls]['case']})"
     roof_dominant = max(roof_all.values(), key=lambda r: r["share"] or 0.0)
+    win_rates = [t / d for t, d in zip(win_tokens, win_dev) if d > 0]
     line = {
         "metric": METRIC,
         "value": slo_tokens / dev_s if dev_s > 0 else 0.0,
@@ -330,12 +384,18 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (BASELINE config-2 trace generator, random-init OPT-13B-shaped bf16 weights)",
-        "config": {"workload": "config2: OPT-13B mixed trace (90% <=1k, 10% 4k-16k prompts), AccelGen policy",
-                   "model": mcfg.name, "parallelism": f"tp{world}", "arrival_rate_rps": rate,
-                   "profile": prof_src, "pivot_forward_size": s_pf, "kv_pool_tokens": num_blocks * 32,
-                   "forward_tokens_per_step": tokens / K, "l2": "inputs larger than L2 (26 GB weights/step)",
-                   "clock": "wall (live)"},
+        "config": {"workload": "config2: OPT-13B mixed trace (90% <=1k, 10% 4k-16k prompts), "
+                               f"{args.policy} policy, steady state",
+                   "model": mcfg.name, "parallelism": f"tp{world}", "tp_backend": args.tp_backend if world > 1 else None,
+                   "arrival_rate_rps": rate, "profile": prof_src, "pivot_forward_size": s_pf,
+                   "kv_pool_tokens": num_blocks * 32, "step": f"{args.window_s:g} s window of serving",
+                   "ramp_s": ramp_s, "forward_tokens_per_step": tokens / K,
+                   "l2": "inputs larger than L2 (26 GB of weights + K/V per forward)", "clock": "wall (live)"},
         "iter_slo_attainment": met / events if events else None,
+        "steady_state": {"ramp_wall_s": ramp_wall, "live_requests": live0, "kv_occupancy": kv0,
+                         "forwards_per_window": len(recs) / K,
+                         "window_value_cv": float(np.std(win_rates) / np.mean(win_rates)) if win_rates else None,
+                         "prompts_credit_unresolved": unresolved},
         "preemptions_in_window": sum(r.preemptions for r in recs),
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,
         "forward_size_pct": {q: int(np.percentile([r.forward_size for r in recs], q)) for q in (10, 50, 90, 99)},
@@ -381,23 +441,26 @@ def cpu_baseline(mcfg, batches, world, budget_s: float = 20.0) -> dict:
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    """The reference's CPU implementation of the path (oracle port) on the host cores."""
+    """The reference's CPU implementation of the path (oracle port) on the host cores, measured the
+    same way: SLO-meeting tokens per window of its own (CPU-timed) clock."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle.bench_cpu import reference_arm
     cfg, prof, prof_src, rate = build_workload(args, world)
-    # bounded CPU sample per step so the whole --steps K --warmup W run ends within a few minutes
-    tok_cap = max(16, min(256, 8192 // max(1, args.steps + args.warmup)))
-    res = reference_arm(cfg, prof, steps=args.steps, warmup=args.warmup, tok_cap=tok_cap)
+    res = reference_arm(cfg, prof, steps=args.steps, warmup=args.warmup, window_s=args.window_s)
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (same trace generator and shapes)",
-        "config": {"workload": "config2: OPT-13B mixed trace, AccelGen policy (oracle restatement)",
-                   "model": cfg.model.name, "parallelism": "cpu", "arrival_rate_rps": rate, "profile": prof_src},
+        "config": {"workload": f"config2: OPT-13B mixed trace, {args.policy} policy (oracle restatement)",
+                   "model": cfg.model.name, "parallelism": "cpu", "arrival_rate_rps": rate, "profile": prof_src,
+                   "step": f"{args.window_s:g} s window of serving (CPU-timed clock)"},
         "impl": "reference",
+        "forward_tokens_per_s": res["forward_tokens_per_s"],
+        "note": "SLO-meeting tokens/s is 0 on the CPU path: a forward takes tens of seconds, every TTFT/TBT "
+                "deadline (<= 0.6 s) is missed; forward_tokens_per_s is its raw forward throughput",
         "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["threads"], "kind": "port",
                          "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -407,6 +470,8 @@ def run_reference(args):
 
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -75,12 +75,15 @@ def time_forward_sample(cfg, batch, budget_s: float = 20.0) -> dict:
             "est_forward_s": total}
 
 
-def reference_arm(run_cfg, profile, steps: int, warmup: int, ramp_s: float = 6.0, tok_cap: int = 256) -> dict:
-    """W + K steps of the reference path on the CPU.  Plans come from the oracle scheduler
-    (virtual clock); each step executes one OPT-13B layer of that step's batch on the CPU
-    oracle, on at most `tok_cap` of its tokens (whole sequences), scaled linearly to all tokens
-    and all layers.  The value is forward tokens / CPU forward time: an upper bound on the
-    reference's SLO-meeting tokens/s (at tens of seconds per iteration no TBT deadline is met)."""
+def reference_arm(run_cfg, profile, steps: int, warmup: int, window_s: float = 1.0, tok_cap: int = 256) -> dict:
+    """The reference's path on the CPU, measured like bench.py's GPU arm.  The oracle scheduler
+    (oracle.sched, the restated AccelGen policy + engine) plans every iteration and its clock advances
+    by the MEASURED CPU time of that iteration's forward (oracle.forward with all host threads; sampled:
+    one of L layers on at most `tok_cap` of the batch's tokens (whole sequences), scaled linearly to all
+    tokens and layers -- the bound that keeps the run to minutes).  Steps are `window_s` windows of that
+    clock after `warmup` windows; SLO-meeting tokens are counted exactly as in bench.py (decode tokens
+    that met TBT, a prompt's chunks iff its first token met TTFT).  At tens of CPU-seconds per forward no
+    deadline is met, so value = 0; the forward tokens/s of the CPU path is reported beside it."""
     from paper_2503_13737_b200 import workload
     from paper_2503_13737_b200.engine import DeviceBatch, synthetic_tokens
     from .sched import OracleScheduler
@@ -90,16 +93,13 @@ def reference_arm(run_cfg, profile, steps: int, warmup: int, ramp_s: float = 6.0
     cfg = run_cfg.model
     trace = workload.generate_trace(run_cfg.trace)
     kv_tok = cfg.kv_bytes_per_token()
-    sch = OracleScheduler(trace, profile, kv_blocks=int(80e9 // (32 * kv_tok)))
-    while sch.clock < ramp_s:
-        sch.step()
+    sch = OracleScheduler(trace, profile, kv_blocks=int(150e9 // (32 * kv_tok)))
     cfg1 = _one_layer(cfg)
     w = _weights(cfg1)
 
     def sample_batch(entry):
         ids, pos, slot, cu, ctx, tabs, lr = [], [], [], [0], [], [], []
         taken = 0
-        full_tokens = sum(c for _, c, _, _ in entry["sel"])
         for rid, c, final, before in entry["sel"]:
             if taken and taken + c > tok_cap:
                 continue
@@ -114,28 +114,49 @@ def reference_arm(run_cfg, profile, steps: int, warmup: int, ramp_s: float = 6.0
         bt = np.zeros((len(tabs), max(map(len, tabs))), np.int32)
         for i, t in enumerate(tabs):
             bt[i, :len(t)] = t
-        b = DeviceBatch(list(range(len(tabs))), np.concatenate(ids), np.concatenate(pos), np.asarray(cu, np.int32),
-                        np.asarray(ctx, np.int32), bt, np.concatenate(slot), np.asarray(lr, np.int32), [])
-        return b, full_tokens
+        return DeviceBatch(list(range(len(tabs))), np.concatenate(ids), np.concatenate(pos),
+                           np.asarray(cu, np.int32), np.asarray(ctx, np.int32), bt, np.concatenate(slot),
+                           np.asarray(lr, np.int32), [])
 
-    done_tokens, cpu_s, sampled = 0, 0.0, 0
-    n = 0
-    while n < warmup + steps:
-        entry = sch.step()
-        if entry is None:
-            continue
-        b, full = sample_batch(entry)
+    stats = {"cpu_s": 0.0, "tokens": 0, "sampled": 0, "forwards": 0}
+
+    def cpu_forward_time(entry):
+        b = sample_batch(entry)
         st, nb = _compact(b)
         o = orc.OracleOPT(cfg1, w, nb)
         t0 = time.perf_counter()
         o.forward(st)
         dt = time.perf_counter() - t0
-        if n >= warmup:
-            est = dt * cfg.num_layers * (full / b.num_tokens)
-            done_tokens += full
-            cpu_s += est
-            sampled += b.num_tokens
-        n += 1
-    return {"value": done_tokens / cpu_s, "ms_per_step": cpu_s / steps * 1e3, "threads": threads,
-            "sample": f"{steps} oracle-scheduled steps; per step 1 of {cfg.num_layers} OPT-13B layers on <= {tok_cap} "
-                      f"tokens ({sampled} sampled of {done_tokens}), scaled linearly to all tokens and layers"}
+        full = sum(c for _, c, _, _ in entry["sel"])
+        est = dt * cfg.num_layers * (full / b.num_tokens)
+        stats["cpu_s"] += est
+        stats["tokens"] += full
+        stats["sampled"] += b.num_tokens
+        stats["forwards"] += 1
+        return est
+
+    sch.clock_fn = cpu_forward_time
+    t_w0, t_w1 = warmup * window_s, (warmup + steps) * window_s
+    while sch.clock < t_w1:
+        if sch.step() is None and sch.nxt >= len(sch.trace) and not sch.queue:
+            break
+    slo_tokens = 0
+    for entry in sch.log:
+        if not (t_w0 <= entry["end"] < t_w1):
+            continue
+        for rid, c, final, before in entry["sel"]:
+            r = sch.reqs[rid]
+            slo = r.spec.slo
+            if before < r.spec.prompt_len:  # prompt chunk: iff the first token met TTFT
+                ok = bool(r.emits) and r.emits[0] - r.spec.arrival_time <= slo.ttft_slo + 1e-12
+            else:  # decode: this emission's gap to the previous one
+                i = r.emits.index(entry["end"])
+                ok = i > 0 and r.emits[i] - r.emits[i - 1] <= slo.tbt_slo + 1e-12
+            slo_tokens += c if ok else 0
+    span = (steps * window_s)
+    return {"value": slo_tokens / span, "ms_per_step": 1e3 * window_s, "threads": threads,
+            "forward_tokens_per_s": stats["tokens"] / stats["cpu_s"] if stats["cpu_s"] else 0.0,
+            "forwards": stats["forwards"],
+            "sample": f"{stats['forwards']} oracle-scheduled forwards over {t_w1:g} s of the CPU clock; each timed "
+                      f"as 1 of {cfg.num_layers} OPT-13B layers on <= {tok_cap} tokens ({stats['sampled']} sampled "
+                      f"of {stats['tokens']}), scaled linearly to all tokens and layers"}

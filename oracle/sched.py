@@ -98,10 +98,12 @@ class Pool:
 class OracleScheduler:
     """Virtual-clock AccelGen simulation over a trace; records every plan."""
 
-    def __init__(self, trace, profile, *, gamma=0.75, max_long=1, slack=0.1, kv_blocks=None, era=True):
+    def __init__(self, trace, profile, *, gamma=0.75, max_long=1, slack=0.1, kv_blocks=None, era=True,
+                 kv_victim="resident_last"):
         self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
         self.p = profile
         self.gamma, self.max_long, self.slack, self.era = gamma, max_long, slack, era
+        self.kv_victim = kv_victim
         self.pool = Pool(kv_blocks if kv_blocks is not None else profile.kvc_capacity_tokens // 32)
         self.t_max = profile.fixed_overhead_s + profile.pivot_time_s * profile.pivot_forward_size / profile.pivot_forward_size
         self.lc = float(profile.pivot_forward_size)
@@ -109,6 +111,8 @@ class OracleScheduler:
         self.p_prob = self.p_max = 0.0
         self.clock, self.nxt, self.stamp = 0.0, 0, 0
         self.queue, self.long_active, self.log = [], set(), []
+        self.reqs = {}         # every admitted request (finished ones leave the queue, not this map)
+        self.clock_fn = None   # optional entry -> elapsed seconds (the CPU-timed reference arm's clock)
         self.preempt_time = {}
 
     # ---- reference arithmetic (sched_core.py:89-146)
@@ -183,8 +187,13 @@ class OracleScheduler:
         free = pool.free
         preempted = []
         while B and (s_f > s_b or used > free):
-            v = max(B, key=lambda m: (tr[m[0].rid], pos[m[0].rid]))
             kv_short = used > free
+            cand = B
+            if kv_short and self.kv_victim == "resident_last":
+                # KV deficit: leave out work that holds no blocks (new / swapped-out) before preempting a
+                # resident request -- brute force: scan the members that are not in the pool
+                cand = [m for m in B if m[0].rid not in pool.tables] or B
+            v = max(cand, key=lambda m: (tr[m[0].rid], pos[m[0].rid]))
             B.remove(v)
             s_f -= v[1]
             used -= v[2]
@@ -241,6 +250,7 @@ class OracleScheduler:
                 est = self.n_ck(s.prompt_len) * self.t_max + s.predicted_output_len * per_tok
                 r.allowance = (s.slo.jct_slo - est) / (self.n_ck(s.prompt_len) + s.predicted_output_len)
             self.queue.append(r)
+            self.reqs[r.rid] = r
 
     def step(self):
         self.admit()
@@ -273,7 +283,11 @@ class OracleScheduler:
             entry["sel"].append((r.rid, c, final, before))
             entry["tables"][r.rid] = list(self.pool.tables[r.rid])
         s_f = sum(c for _, c, _ in chosen)
-        self.clock = start + self.iter_time(s_f, [(c, before) for _, c, _, before in entry["sel"]])
+        if self.clock_fn is not None:
+            self.clock = start + self.clock_fn(entry)
+        else:
+            self.clock = start + self.iter_time(s_f, [(c, before) for _, c, _, before in entry["sel"]])
+        entry["start"], entry["end"] = start, self.clock
         now = self.clock
         done = set()
         for r, c, blk in chosen:

@@ -164,7 +164,10 @@ class IterationRecord:
     wall_s: float = 0.0
     events: int = 0
     events_met: int = 0
-    slo_tokens: int = 0   # tokens of this forward whose request met (or is on track for) its deadline
+    slo_tokens: int = 0   # tokens of this forward already known to meet their deadline (decodes, final chunks)
+    # non-final prompt chunks (request id, tokens): they meet the SLO iff the request's first token (the
+    # final chunk) meets TTFT, known only later -- resolve with Engine.prefill_met()
+    pending_prefill: list = field(default_factory=list)
     host_pre_s: float = 0.0   # admit + order + plan + allocate + pack (before executor.execute)
     host_post_s: float = 0.0  # emission + re-enqueue (after executor.execute)
 
@@ -304,6 +307,16 @@ class Engine:
 
     def done(self) -> bool:
         return self._next_arrival >= len(self.trace) and not self.queue
+
+    def prefill_met(self, request_id: int) -> bool | None:
+        """Whether request_id's prompt tokens meet their SLO: TTFT of the first token (online) or the
+        JCT deadline (offline, judged at the first token's time); None while the prompt is unfinished."""
+        rec = self.metrics.requests[request_id]
+        if rec.first_token_time is None:
+            return None
+        slo = rec.spec.slo
+        limit = slo.jct_slo if slo.kind is SLOKind.OFFLINE else slo.ttft_slo
+        return rec.first_token_time - rec.spec.arrival_time <= limit + 1e-12
 
     # -------------------------------------------------------------- one iteration
     def step(self) -> IterationRecord | None:
@@ -465,9 +478,9 @@ class Engine:
                 it.num_decode += 1
                 e.seq_len += 1
             if not sel.is_final_chunk:
-                # non-final chunk: same TTFT clock, back in the queue
-                on_track = spec.slo.kind is SLOKind.OFFLINE or now - spec.arrival_time <= spec.slo.ttft_slo
-                it.slo_tokens += sel.chunk_len if on_track else 0
+                # non-final chunk: same TTFT clock, back in the queue; its tokens count as SLO-meeting only
+                # if the final chunk later meets TTFT (offline requests: JCT, resolved the same way)
+                it.pending_prefill.append((rid, sel.chunk_len))
                 e.phase = Phase.PROMPT_PENDING
                 e.seq = self._stamp_next()
                 continue

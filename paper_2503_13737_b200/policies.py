@@ -16,7 +16,10 @@ ambiguity pinned once (SURVEY §8c'):
   "retained in the batch as much as possible", PAPER §4.4).  While S_f > S_b or B's block demand
   exceeds the free blocks, the member with max T_r (ties: later queue position) leaves B; only
   when the KV blocks are the deficit and it holds blocks is it preempted (swapped out, freeing
-  them) -- a token-budget deficit merely defers it with its KV resident.
+  them) -- a token-budget deficit merely defers it with its KV resident.  Under a KV deficit the
+  default ``kv_victim="resident_last"`` first drops members holding no blocks (new prompts,
+  swapped-out requests), so admitting work never evicts a resident request; ``"max_tr"`` is the
+  paper-literal rule (evict/readmit churn once the pool is full).
 * Algorithm 2 (select_requests): window = non-urgent entries with T_r <= T_r^1 + gamma.  Every
   pending prompt in the window (short or long, PAPER §4.2 "regardless of their associated
   requests") is offered as a chunk min(remaining, A_c, tokens fitting A_m); TG / preempted TG
@@ -84,6 +87,7 @@ class PolicyConfig:
     urgency_slack: float = DEFAULT_URGENCY_SLACK
     era: bool = True
     fcfs_budget: int | None = None    # PagedFcfs / Orca forward cap (None -> max(S_pf, 16384))
+    kv_victim: str = "resident_last"  # KV-deficit victim rule: "resident_last" or the paper-literal "max_tr"
 
     def __post_init__(self):
         if self.policy not in POLICIES:
@@ -94,6 +98,8 @@ class PolicyConfig:
             raise ConfigError("budget_cap must be >= 1")
         if self.max_concurrent_long < 1:
             raise ConfigError("max_concurrent_long must be >= 1")
+        if self.kv_victim not in ("resident_last", "max_tr"):
+            raise ConfigError("kv_victim must be 'resident_last' or 'max_tr'")
 
 
 def token_budget(slo_min: float, profile: ModelProfile, cfg: PolicyConfig) -> int:
@@ -264,17 +270,23 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
     free = pool.free_blocks
     preempted: list[int] = []
     if members and (s_f > s_b or used > free):
-        # repeatedly drop the member with max T_r (ties: later queue position) until B fits:
-        # equivalent to walking the members in descending (T_r, position) order
-        order = sorted(range(len(members)),
-                       key=lambda i: (t_r[members[i][0].request_id], position[members[i][0].request_id]),
-                       reverse=True)
+        # repeatedly drop the member with max T_r (ties: later queue position) until B fits.  With
+        # kv_victim="resident_last" a KV deficit first drops members that hold no blocks (prompts not yet
+        # started, swapped-out requests awaiting readmission): admitting new work never evicts a resident
+        # request's KV to host -- the evict/readmit churn the paper-literal rule ("max_tr") produces once
+        # the pool is full
+        def rank(i):
+            return t_r[members[i][0].request_id], position[members[i][0].request_id]
+        alive = list(range(len(members)))
         dropped = set()
-        for i in order:
-            if not (s_f > s_b or used > free):
-                break
-            e, c, blk = members[i]
+        while alive and (s_f > s_b or used > free):
             kv_short = used > free
+            cand = alive
+            if kv_short and cfg.kv_victim == "resident_last":
+                cand = [i for i in alive if not pool.is_resident(members[i][0].request_id)] or alive
+            i = max(cand, key=rank)
+            alive.remove(i)
+            e, c, blk = members[i]
             dropped.add(i)
             s_f -= c
             used -= blk
@@ -351,6 +363,13 @@ def baseline_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
             if c < 1:
                 break
             add(e, c, step_blocks(e, c, pool))
+        if not plan.selections and tg:
+            # pool exhausted by decodes that each need a new block: preempt the latest arrival, as vLLM /
+            # Sarathi do (without it the baseline deadlocks once the KV pool is full)
+            victim = max((e for e in tg if pool.is_resident(e.request_id)),
+                         key=lambda e: (e.request.arrival_time, e.request_id), default=None)
+            if victim is not None:
+                plan.preempted.append(victim.request_id)
     elif cfg.policy == "paged_fcfs":
         # vLLM FCFS: running decodes, then whole prompts; stop at the first prompt that does not fit
         s_b = _fcfs_budget(ctx.profile, cfg)

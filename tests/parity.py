@@ -22,6 +22,7 @@ class Tally:
         self.worst = self.floor = self.sum_d = self.sum_f = 0.0
         self.agree = self.exempt = self.total = 0
         self.rows = []
+        self.oracle_flips = 0  # rows whose greedy token differs between the fp32 and fp64 oracles
 
     def add(self, dev_logits, dev_tokens, ref_logits, ref_tokens, ref64_logits=None):
         n = ref_logits.shape[0]
@@ -34,6 +35,7 @@ class Tally:
             f = (ref64_logits.float() - ref_logits.float()).abs()
             self.floor = max(self.floor, f.max().item())
             self.sum_f += f.mean().item() * n
+            self.oracle_flips += int((ref64_logits.float().argmax(-1).numpy() != np.asarray(ref_tokens[:n])).sum())
         same = np.asarray(dev_tokens[:n]) == np.asarray(ref_tokens[:n])
         top2 = ref_logits.float().topk(2, dim=-1).values
         self.rows += list(zip(same.tolist(), (top2[:, 0] - top2[:, 1]).tolist()))
@@ -47,7 +49,7 @@ class Tally:
         mean_d, mean_f = self.sum_d / max(self.total, 1), self.sum_f / max(self.total, 1)
         print(f"{label}: max|dlogit|={self.worst:.4g} (bound {bound:.4g}, fp32-vs-fp64 oracle floor "
               f"{self.floor:.4g}) mean|dlogit|={mean_d:.3g} (floor mean {mean_f:.3g}) tokens {agree}/{self.total} "
-              f"(agreement {rate:.4f}, near-tie exempt {exempt})")
+              f"(agreement {rate:.4f}, near-tie exempt {exempt}; fp32-vs-fp64 oracle token flips {self.oracle_flips})")
         assert self.worst <= bound
         if self.floor > 0:
             assert mean_d <= FLOOR_FACTOR * mean_f + 1e-4

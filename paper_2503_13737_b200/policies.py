@@ -275,17 +275,23 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
         # started, swapped-out requests awaiting readmission): admitting new work never evicts a resident
         # request's KV to host -- the evict/readmit churn the paper-literal rule ("max_tr") produces once
         # the pool is full
-        def rank(i):
-            return t_r[members[i][0].request_id], position[members[i][0].request_id]
-        alive = list(range(len(members)))
+        # victims in descending (T_r, position) order; residency does not change inside this loop, so the
+        # "max over the non-resident members, else over all" choice is two cursors over presorted lists
+        order = sorted(range(len(members)), key=lambda i: (t_r[members[i][0].request_id],
+                                                            position[members[i][0].request_id]), reverse=True)
+        nonres = [i for i in order if not pool.is_resident(members[i][0].request_id)]
+        p_all = p_nonres = 0
         dropped = set()
-        while alive and (s_f > s_b or used > free):
+        while len(dropped) < len(members) and (s_f > s_b or used > free):
             kv_short = used > free
-            cand = alive
-            if kv_short and cfg.kv_victim == "resident_last":
-                cand = [i for i in alive if not pool.is_resident(members[i][0].request_id)] or alive
-            i = max(cand, key=rank)
-            alive.remove(i)
+            while p_nonres < len(nonres) and nonres[p_nonres] in dropped:
+                p_nonres += 1
+            if kv_short and cfg.kv_victim == "resident_last" and p_nonres < len(nonres):
+                i = nonres[p_nonres]
+            else:
+                while order[p_all] in dropped:
+                    p_all += 1
+                i = order[p_all]
             e, c, blk = members[i]
             dropped.add(i)
             s_f -= c
@@ -378,12 +384,19 @@ def baseline_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
             blk = step_blocks(e, 1, pool)
             if s_f + 1 <= s_b and blk <= free:
                 add(e, 1, blk)
+        first = True
         for e in prompts:
             c = e.remaining_prompt_tokens
             blk = step_blocks(e, c, pool)
-            if s_f + c > s_b or blk > free:
+            # a prompt longer than the budget runs as the only prompt of its step (vLLM requires
+            # max_num_batched_tokens >= max_model_len; without this the FCFS head blocks forever)
+            over = s_f + c > s_b and not (first and c > s_b)
+            if over or blk > free:
                 break
             add(e, c, blk)
+            first = False
+            if c > s_b:
+                break
         if not plan.selections and tg:
             # pool exhausted by decodes without headroom: preempt the latest arrival (vLLM policy)
             victim = max((e for e in tg if pool.is_resident(e.request_id)),
@@ -409,11 +422,12 @@ def baseline_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
                 continue
             c = e.remaining_prompt_tokens
             blk = step_blocks(e, c, pool)
-            if s_f + c > s_b or blk > free:
+            if (s_f + c > s_b and not (s_f == 0 and c > s_b)) or blk > free:  # over-budget prompt: alone
                 break
             add(e, c, blk)
             n_live += 1
     plan.forward_size = s_f
+    plan.token_budget = max(plan.token_budget, s_f)  # an over-budget prompt alone stretches its step's budget
     return plan
 
 

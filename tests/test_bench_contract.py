@@ -18,7 +18,9 @@ def test_reference_arm_json_contract():
               "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["steps"] == 1 and d["n_gpus"] == 1
-    assert d["higher_is_better"] is True and d["value"] > 0
+    # the CPU path meets no TTFT/TBT deadline (a forward takes CPU-seconds), so its SLO-meeting rate is 0;
+    # its raw forward throughput is reported beside it
+    assert d["higher_is_better"] is True and d["value"] >= 0 and d["forward_tokens_per_s"] > 0
     assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
     assert d["cpu_baseline"]["kind"] == "port"
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])

@@ -56,6 +56,10 @@ def parse_args():
     ap.add_argument("--kv-gb", type=float, default=None,
                     help="KV pool per GPU (GB); default: the HBM left after weights and a 12 GB reserve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kv-watermark", type=float, default=0.1,
+                    help="AccelGen admission watermark (fraction of the KV pool kept for decode growth)")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="synchronous engine (plan, forward, emit in turn) instead of planning step k+1 during k")
     return ap.parse_args()
 
 
@@ -226,7 +230,9 @@ def run_ours(args):
 
     trace = workload.generate_trace(cfg.trace)
     executor = TP.TPLeader(ex, group) if world > 1 else ex
-    eng = Engine(trace, prof, PolicyConfig(policy=args.policy), executor, clock="wall", kv_blocks=num_blocks)
+    pipeline = world == 1 and not args.no_pipeline  # TP followers mirror synchronous steps
+    eng = Engine(trace, prof, PolicyConfig(policy=args.policy, kv_watermark=args.kv_watermark), executor,
+                 clock="wall", kv_blocks=num_blocks, pipeline=pipeline)
 
     def serve_until(t_end):
         its = []
@@ -249,12 +255,18 @@ def run_ours(args):
 
     # ---------------- timed region: exactly K windows of serving
     batches = []
-    orig_exec = ex.execute
+    orig_exec, orig_submit = ex.execute, getattr(ex, "submit", None)
 
     def recording_exec(b):
         batches.append(b)
         return orig_exec(b)
+
+    def recording_submit(b, feed=None):
+        batches.append(b)
+        return orig_submit(b, feed)
     ex.execute = recording_exec
+    if orig_submit is not None:
+        ex.submit = recording_submit
     peaks = load_peaks()
     ex.set_roofline_peaks(peaks["tensor_sustained"], peaks["hbm"])
     ex.set_profiling(False)  # the timed windows run un-instrumented; kernel classes come from a replay
@@ -283,6 +295,8 @@ def run_ours(args):
         executor.mark(0)
         dist.barrier()
     ex.execute = orig_exec
+    if orig_submit is not None:
+        ex.submit = orig_submit
     recs = [it for w in windows for it in w]
     dev_s = sum(r.device_s for r in recs)
     launches_timed = ex.launches - launches0
@@ -294,6 +308,7 @@ def run_ours(args):
     t_res = eng.clock
     while any(eng.prefill_met(r) is None for r in pending) and not eng.done() and eng.clock < t_res + 120:
         eng.step()
+    eng.flush()
     unresolved = sum(eng.prefill_met(r) is None for r in pending)
 
     def credited(it):
@@ -390,13 +405,15 @@ def run_ours(args):
                    "arrival_rate_rps": rate, "profile": prof_src, "pivot_forward_size": s_pf,
                    "kv_pool_tokens": num_blocks * 32, "step": f"{args.window_s:g} s window of serving",
                    "ramp_s": ramp_s, "forward_tokens_per_step": tokens / K,
-                   "l2": "inputs larger than L2 (26 GB of weights + K/V per forward)", "clock": "wall (live)"},
+                   "l2": "inputs larger than L2 (26 GB of weights + K/V per forward)", "clock": "wall (live)",
+                   "pipelined_host": pipeline, "kv_watermark": args.kv_watermark},
         "iter_slo_attainment": met / events if events else None,
         "steady_state": {"ramp_wall_s": ramp_wall, "live_requests": live0, "kv_occupancy": kv0,
                          "forwards_per_window": len(recs) / K,
                          "window_value_cv": float(np.std(win_rates) / np.mean(win_rates)) if win_rates else None,
                          "prompts_credit_unresolved": unresolved},
         "preemptions_in_window": sum(r.preemptions for r in recs),
+        "swap_gb_total": getattr(ex, "swap_bytes", 0) / 1e9,
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,
         "forward_size_pct": {q: int(np.percentile([r.forward_size for r in recs], q)) for q in (10, 50, 90, 99)},
         "token_events": events,

@@ -39,6 +39,7 @@ extern "C" {
 #define AG_EALLOC 3  /* capacity exceeded (tokens, sequences, workspace) */
 #define AG_EFAULT 4  /* internal invariant violation (reference: EngineFault, errors.py:28-32) */
 #define AG_ENCCL 5   /* NCCL error (tensor parallel) */
+#define AG_ESTATE 6  /* call-order violation, e.g. a third asynchronous step (reference: StateError, errors.py:24) */
 
 typedef struct ag_model ag_model; /* opaque */
 
@@ -147,6 +148,22 @@ AG_API int32_t ag_model_init_tp_host(ag_model* m, ag_host_collective_fn fn, void
  * forward alone (metadata already resident, before the D2H).  Synchronises `stream`. */
 AG_API int32_t ag_model_forward(ag_model* m, const ag_step* step, int32_t* out_tokens, float* logits_out,
                          float* device_ms, void* stream);
+
+/* Asynchronous steps (the host plans step k+1 while the GPU runs step k).  ag_model_submit validates
+ * and stages the step like ag_model_forward, enqueues the forward and the D2H of its next-token ids on
+ * `stream` and returns; at most two steps are in flight.  feed_pairs = n_feed (token index, logit row)
+ * int32 pairs: decode token `token index` of this step takes the next-token id that the PREVIOUS
+ * submitted step emits at `logit row` (autoregressive input resolved on the device, no host round
+ * trip).  ag_model_wait completes the oldest step in flight: its ids into out_tokens (cap entries),
+ * its CUDA-event forward time, and the time of its last kernel in ms after the ag_model_clock_ref
+ * event (which records an event on `stream` and waits for it, so the host can map device completion
+ * times onto its own clock).  Replaces the same clock advance as ag_model_forward. */
+AG_API int32_t ag_model_submit(ag_model* m, const ag_step* step, const int32_t* feed_pairs, int32_t n_feed,
+                               float* logits_out, void* stream);
+AG_API int32_t ag_model_wait(ag_model* m, int32_t* out_tokens, int32_t cap, float* device_ms,
+                             double* end_ms_since_ref);
+AG_API int32_t ag_model_clock_ref(ag_model* m, void* stream);
+AG_API int32_t ag_model_inflight(ag_model* m);
 
 /* Same forward, asynchronous, with all metadata already packed in device memory by
  * ag_model_stage_step (used to time the kernels with inputs resident in HBM). */

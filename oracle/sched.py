@@ -99,11 +99,12 @@ class OracleScheduler:
     """Virtual-clock AccelGen simulation over a trace; records every plan."""
 
     def __init__(self, trace, profile, *, gamma=0.75, max_long=1, slack=0.1, kv_blocks=None, era=True,
-                 kv_victim="resident_last"):
+                 kv_victim="resident_last", kv_watermark=0.0):
         self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
         self.p = profile
         self.gamma, self.max_long, self.slack, self.era = gamma, max_long, slack, era
         self.kv_victim = kv_victim
+        self.kv_watermark = kv_watermark
         self.pool = Pool(kv_blocks if kv_blocks is not None else profile.kvc_capacity_tokens // 32)
         self.t_max = profile.fixed_overhead_s + profile.pivot_time_s * profile.pivot_forward_size / profile.pivot_forward_size
         self.lc = float(profile.pivot_forward_size)
@@ -186,10 +187,19 @@ class OracleScheduler:
             used += blk
         free = pool.free
         preempted = []
-        while B and (s_f > s_b or used > free):
+        wm = int(self.kv_watermark * pool.total)
+
+        def used_new():  # blocks of members holding none (new prompts, readmissions)
+            return sum(m[2] for m in B if m[0].rid not in pool.tables)
+
+        def wm_short():
+            return wm > 0 and used_new() > 0 and used > free - wm
+        while B and (s_f > s_b or used > free or wm_short()):
             kv_short = used > free
             cand = B
-            if kv_short and self.kv_victim == "resident_last":
+            if not kv_short and wm_short() and s_f <= s_b:
+                cand = [m for m in B if m[0].rid not in pool.tables]
+            elif kv_short and self.kv_victim == "resident_last":
                 # KV deficit: leave out work that holds no blocks (new / swapped-out) before preempting a
                 # resident request -- brute force: scan the members that are not in the pool
                 cand = [m for m in B if m[0].rid not in pool.tables] or B
@@ -217,16 +227,17 @@ class OracleScheduler:
                 for i, r in enumerate(win):
                     if r.rid in taken:
                         continue
+                    room = a_m if r.rid in pool.tables else a_m - wm * pool.b
                     if self.prompt_left(r):
                         if self.era_blocked(r, active):
                             continue
-                        c = min(r.remaining, a_c, pool.fit(r, a_m // pool.b))
+                        c = min(r.remaining, a_c, pool.fit(r, max(0, room) // pool.b))
                         if c < 1:
                             continue
                     else:
                         c = 1
                     blk = pool.need(r, c)
-                    if c <= a_c and blk * pool.b <= a_m:
+                    if c <= a_c and blk * pool.b <= room:
                         cands.append(((a_c - c) ** 2 + (a_m - blk * pool.b) ** 2, i, r, c, blk))
                 if not cands:
                     break

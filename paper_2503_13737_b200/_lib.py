@@ -9,11 +9,11 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-from .errors import AllocationError, EngineFault, ValidationError
+from .errors import AllocationError, EngineFault, StateError, ValidationError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libaccelgen_b200.so"
 
-AG_OK, AG_EINVAL, AG_ECUDA, AG_EALLOC, AG_EFAULT, AG_ENCCL = range(6)
+AG_OK, AG_EINVAL, AG_ECUDA, AG_EALLOC, AG_EFAULT, AG_ENCCL, AG_ESTATE = range(7)
 
 # kernel classes of ag_model_get_profile (include/accelgen_b200.h AG_K_*)
 PROF_CLASSES = ("embed", "layernorm", "qkv_gemm", "attention", "out_gemm", "fc1_gemm", "fc2_gemm", "lmhead_gemm",
@@ -65,6 +65,10 @@ _SIGS = {
     "ag_model_init_tp": (i32, [vp, vp]),
     "ag_model_init_tp_host": (i32, [vp, vp, vp]),
     "ag_model_forward": (i32, [vp, C.POINTER(Step), vp, vp, P_f32, vp]),
+    "ag_model_submit": (i32, [vp, C.POINTER(Step), vp, i32, vp, vp]),
+    "ag_model_wait": (i32, [vp, vp, i32, P_f32, C.POINTER(C.c_double)]),
+    "ag_model_clock_ref": (i32, [vp, vp]),
+    "ag_model_inflight": (i32, [vp]),
     "ag_model_stage_step": (i32, [vp, C.POINTER(Step), vp]),
     "ag_model_forward_staged": (i32, [vp, vp, vp, vp]),
     "ag_model_set_profiling": (i32, [vp, i32]),
@@ -123,4 +127,6 @@ def check(rc: int) -> None:
         raise ValidationError(msg)
     if rc == AG_EALLOC:
         raise AllocationError(msg)
+    if rc == AG_ESTATE:
+        raise StateError(msg)
     raise EngineFault(f"device step failed (code {rc}): {msg}")

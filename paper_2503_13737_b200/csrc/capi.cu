@@ -246,6 +246,21 @@ struct ag_model {
   uint8_t* coll_host = nullptr;
   size_t coll_host_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // asynchronous steps (ag_model_submit / ag_model_wait): two in-flight slots, each with its own pinned
+  // metadata, next-token ids (device + pinned host), decode-feed pairs and events; the device metadata
+  // buffer is shared (stream order: step k+1's H2D runs after step k's kernels)
+  struct AsyncSlot {
+    uint8_t* meta_host = nullptr;
+    int32_t* out_tok = nullptr;
+    int32_t* tok_host = nullptr;
+    int32_t* feed_host = nullptr;
+    cudaEvent_t start = nullptr, end = nullptr, done = nullptr;
+    int n_logit = 0;
+    bool active = false;
+  } aslot[2];
+  int32_t* feed_dev = nullptr;
+  int64_t n_submit = 0, n_wait = 0;
+  cudaEvent_t ev_ref = nullptr;
   // per-kernel-class profiling (CUDA events around every launch of one forward)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_events;
@@ -553,11 +568,24 @@ void ag_model_destroy(ag_model* m) {
                  m->splitk_ws, m->acc32, m->acc_big};
   for (void* p : dev)
     if (p) cudaFree(p);
+  if (m->aslot[0].meta_host) m->meta_host = m->aslot[0].meta_host;  // slot 1's buffer is freed below
   if (m->meta_host) cudaFreeHost(m->meta_host);
   if (m->coll_host) cudaFreeHost(m->coll_host);
   if (m->tok_host) cudaFreeHost(m->tok_host);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
+  for (int i = 1; i < 2; ++i) {  // slot 0 aliases meta_host / out_tok / tok_host
+    if (m->aslot[i].meta_host) cudaFreeHost(m->aslot[i].meta_host);
+    if (m->aslot[i].tok_host) cudaFreeHost(m->aslot[i].tok_host);
+    if (m->aslot[i].out_tok) cudaFree(m->aslot[i].out_tok);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (m->aslot[i].feed_host) cudaFreeHost(m->aslot[i].feed_host);
+    for (cudaEvent_t e : {m->aslot[i].start, m->aslot[i].end, m->aslot[i].done})
+      if (e) cudaEventDestroy(e);
+  }
+  if (m->feed_dev) cudaFree(m->feed_dev);
+  if (m->ev_ref) cudaEventDestroy(m->ev_ref);
   delete m;
 }
 
@@ -1167,6 +1195,7 @@ int64_t ag_model_last_h2d_bytes(ag_model* m) { return m ? m->h2d_last : -1; }
 int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, float* logits_out, float* device_ms,
                          void* stream) {
   if (!m || !st) return fail(AG_EINVAL, "null argument");
+  if (m->n_submit != m->n_wait) return fail(AG_ESTATE, "ag_model_forward with asynchronous steps in flight");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   AG_TRY(ag_model_stage_step(m, st, stream));
   AG_CUDA(cudaEventRecord(m->ev0, s));
@@ -1180,6 +1209,92 @@ int32_t ag_model_forward(ag_model* m, const ag_step* st, int32_t* out_tokens, fl
   if (out_tokens && m->n_logit > 0) std::memcpy(out_tokens, m->tok_host, sizeof(int32_t) * m->n_logit);
   return AG_OK;
 }
+
+int32_t ag_model_clock_ref(ag_model* m, void* stream) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  if (!m->ev_ref) AG_CUDA(cudaEventCreate(&m->ev_ref));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  AG_CUDA(cudaEventRecord(m->ev_ref, s));
+  AG_CUDA(cudaEventSynchronize(m->ev_ref));
+  return AG_OK;
+}
+
+int32_t ag_model_submit(ag_model* m, const ag_step* st, const int32_t* feed_pairs, int32_t n_feed, float* logits_out,
+                        void* stream) {
+  if (!m || !st) return fail(AG_EINVAL, "null argument");
+  if (m->prof_on) return fail(AG_ESTATE, "per-kernel profiling needs the synchronous ag_model_forward");
+  if (n_feed < 0 || n_feed > st->num_tokens || (n_feed > 0 && !feed_pairs)) return fail(AG_EINVAL, "bad feed");
+  if (n_feed > 0 && m->n_submit == 0) return fail(AG_ESTATE, "decode feed without a previous step");
+  const int k = static_cast<int>(m->n_submit & 1);
+  ag_model::AsyncSlot& a = m->aslot[k];
+  if (a.active) return fail(AG_ESTATE, "two asynchronous steps already in flight: ag_model_wait first");
+  const ag_model_config& c = m->cfg;
+  const size_t Sq = static_cast<size_t>(c.max_seqs);
+  if (!a.start) {  // lazily: slot 0 aliases the synchronous path's buffers
+    if (k == 0) {
+      a.meta_host = m->meta_host;
+      a.out_tok = m->out_tok;
+      a.tok_host = m->tok_host;
+    } else {
+      if (cudaMallocHost(&a.meta_host, m->meta_cap) != cudaSuccess) return fail(AG_EALLOC, "pinned alloc");
+      if (cudaMallocHost(&a.tok_host, Sq * sizeof(int32_t)) != cudaSuccess) return fail(AG_EALLOC, "pinned alloc");
+      AG_CUDA(cudaMalloc(&a.out_tok, Sq * sizeof(int32_t)));
+    }
+    if (cudaMallocHost(&a.feed_host, 2 * sizeof(int32_t) * c.max_tokens) != cudaSuccess)
+      return fail(AG_EALLOC, "pinned alloc");
+    if (!m->feed_dev) AG_CUDA(cudaMalloc(&m->feed_dev, 2 * 2 * sizeof(int32_t) * c.max_tokens));
+    AG_CUDA(cudaEventCreate(&a.start));
+    AG_CUDA(cudaEventCreate(&a.end));
+    AG_CUDA(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+  }
+  for (int i = 0; i < n_feed; ++i) {
+    const int dst = feed_pairs[2 * i], src = feed_pairs[2 * i + 1];
+    if (dst < 0 || dst >= st->num_tokens || src < 0 || src >= m->aslot[k ^ 1].n_logit)
+      return fail(AG_EINVAL, "decode feed pair out of range");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  m->meta_host = a.meta_host;
+  AG_TRY(ag_model_stage_step(m, st, stream));
+  if (n_feed > 0) {
+    int32_t* fd = m->feed_dev + 2 * static_cast<size_t>(c.max_tokens) * k;
+    std::memcpy(a.feed_host, feed_pairs, 2 * sizeof(int32_t) * n_feed);
+    AG_CUDA(cudaMemcpyAsync(fd, a.feed_host, 2 * sizeof(int32_t) * n_feed, cudaMemcpyHostToDevice, s));
+    AG_CUDA(ag::launch_feed_tokens(const_cast<int32_t*>(m->d_ids), fd, n_feed, m->aslot[k ^ 1].out_tok, s));
+    m->h2d_last += 8 * n_feed;
+  }
+  AG_CUDA(cudaEventRecord(a.start, s));
+  AG_TRY(ag_model_forward_staged(m, a.out_tok, logits_out, stream));
+  AG_CUDA(cudaEventRecord(a.end, s));
+  if (m->n_logit > 0)
+    AG_CUDA(cudaMemcpyAsync(a.tok_host, a.out_tok, sizeof(int32_t) * m->n_logit, cudaMemcpyDeviceToHost, s));
+  AG_CUDA(cudaEventRecord(a.done, s));
+  a.n_logit = m->n_logit;
+  a.active = true;
+  ++m->n_submit;
+  return AG_OK;
+}
+
+int32_t ag_model_wait(ag_model* m, int32_t* out_tokens, int32_t cap, float* device_ms, double* end_ms_since_ref) {
+  if (!m) return fail(AG_EINVAL, "null model");
+  if (m->n_wait == m->n_submit) return fail(AG_ESTATE, "no asynchronous step in flight");
+  ag_model::AsyncSlot& a = m->aslot[m->n_wait & 1];
+  AG_CUDA(cudaEventSynchronize(a.done));
+  if (device_ms) AG_CUDA(cudaEventElapsedTime(device_ms, a.start, a.end));
+  if (end_ms_since_ref) {
+    float ms = -1.f;
+    if (m->ev_ref) AG_CUDA(cudaEventElapsedTime(&ms, m->ev_ref, a.end));
+    *end_ms_since_ref = ms;
+  }
+  if (out_tokens && a.n_logit > 0) {
+    if (cap < a.n_logit) return fail(AG_EINVAL, "out_tokens too small");
+    std::memcpy(out_tokens, a.tok_host, sizeof(int32_t) * a.n_logit);
+  }
+  a.active = false;
+  ++m->n_wait;
+  return AG_OK;
+}
+
+int32_t ag_model_inflight(ag_model* m) { return m ? static_cast<int32_t>(m->n_submit - m->n_wait) : -1; }
 
 // ---------------------------------------------------------------- standalone kernels
 int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias, const void* residual,

@@ -477,6 +477,21 @@ cudaError_t launch_fill_hash(__nv_bfloat16* x, int64_t n, uint32_t seed, float s
   return cudaGetLastError();
 }
 
+// decode inputs fed from the previous step's next-token ids without a host round trip (asynchronous
+// steps, ag_model_submit): ids[pairs[2i]] = prev_out[pairs[2i+1]]
+__global__ void feed_tokens_kernel(int32_t* __restrict__ ids, const int32_t* __restrict__ pairs, int n,
+                                   const int32_t* __restrict__ prev_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ids[pairs[2 * i]] = prev_out[pairs[2 * i + 1]];
+}
+
+cudaError_t launch_feed_tokens(int32_t* ids, const int32_t* pairs, int n, const int32_t* prev_out,
+                               cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  feed_tokens_kernel<<<(n + 255) / 256, 256, 0, stream>>>(ids, pairs, n, prev_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,
                          const __nv_bfloat16* pos_emb, int pos_offset, int rows, int hidden, int vocab,
                          int max_pos_rows, __nv_bfloat16* out, cudaStream_t stream) {

@@ -58,6 +58,8 @@ GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats);
 cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& ep, cudaStream_t stream);
 
 // embed: out[r] = tok_emb[ids[r]] + pos_emb[positions[r] + pos_offset]
+cudaError_t launch_feed_tokens(int32_t* ids, const int32_t* pairs, int n, const int32_t* prev_out,
+                               cudaStream_t stream);
 cudaError_t launch_embed(const int32_t* ids, const int32_t* positions, const __nv_bfloat16* tok_emb,
                          const __nv_bfloat16* pos_emb, int pos_offset, int rows, int hidden,
                          int vocab, int max_pos_rows, __nv_bfloat16* out, cudaStream_t stream);

@@ -86,6 +86,7 @@ class StepResult:
     device_s: float = 0.0
     wall_s: float = 0.0
     logits: object = None  # optional fp32 [n_logit, V] (parity mode)
+    end_s: float | None = None  # host perf_counter time the forward completed at (asynchronous steps)
 
 
 class Executor(Protocol):
@@ -260,9 +261,11 @@ class Engine:
     def __init__(self, trace: list[RequestSpec], profile: ModelProfile, policy: PolicyConfig | None = None,
                  executor: Executor | None = None, *, clock: str = "virtual", kv_blocks: int | None = None,
                  block_size: int = 32, horizon_s: float = math.inf, per_token_swap_cost_s: float = 0.0,
-                 check_invariants: bool = False, autoregressive: bool = True):
+                 check_invariants: bool = False, autoregressive: bool = True, pipeline: bool = False):
         if clock not in ("virtual", "device", "wall"):
             raise ValueError(f"unknown clock {clock!r}")
+        if pipeline and (clock != "wall" or not hasattr(executor, "submit")):
+            raise ValueError("pipeline=True needs clock='wall' and an executor with submit()/wait()")
         self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
         self.profile = profile
         self.cfg = policy or PolicyConfig()
@@ -288,6 +291,15 @@ class Engine:
         self.plans: list[BatchPlan] = []      # kept for parity tests (scheduler decisions)
         self.tables: list[dict] = []          # per-step block tables (physical ids)
         self.keep_history = False
+        # pipelined wall clock: step k+1 is planned and submitted while the device runs step k
+        self.pipeline = pipeline
+        self._inflight: dict | None = None
+        self._origin: float | None = None   # perf_counter time of engine time 0 (minus idle jumps)
+        self._offset = 0.0                  # idle jumps (empty queue: the clock skips to the next arrival)
+        self._sched_emitted: dict[int, int] = {}
+        self._pending_tok: dict[int, tuple[int, int]] = {}  # rid -> (step id, logit row) of a token in flight
+        self._last_end = 0.0
+        self._n_submitted = 0
 
     # -------------------------------------------------------------- helpers
     def _stamp_next(self) -> int:
@@ -306,7 +318,7 @@ class Engine:
             self.metrics.requests[spec.id] = RequestRecord(spec)
 
     def done(self) -> bool:
-        return self._next_arrival >= len(self.trace) and not self.queue
+        return self._next_arrival >= len(self.trace) and not self.queue and self._inflight is None
 
     def prefill_met(self, request_id: int) -> bool | None:
         """Whether request_id's prompt tokens meet their SLO: TTFT of the first token (online) or the
@@ -320,6 +332,8 @@ class Engine:
 
     # -------------------------------------------------------------- one iteration
     def step(self) -> IterationRecord | None:
+        if self.pipeline:
+            return self._step_pipelined()
         t_step0 = time.perf_counter()
         self._admit()
         if not self.queue:
@@ -517,6 +531,241 @@ class Engine:
         self.metrics.iterations.append(it)
         return it
 
+    # -------------------------------------------------------------- pipelined iteration (wall clock)
+    def _now(self) -> float:
+        return time.perf_counter() - self._origin + self._offset
+
+    def flush(self) -> IterationRecord | None:
+        """Complete the step still on the device (pipelined mode)."""
+        if self._inflight is None:
+            return None
+        prev, self._inflight = self._inflight, None
+        return self._complete(prev)
+
+    def _step_pipelined(self) -> IterationRecord | None:
+        """One iteration with the host one step ahead of the device (wall clock).
+
+        Plan -> allocate -> pack -> ``executor.submit`` (returns at once) -> apply the step's state
+        transitions optimistically (chunk progress, TG re-enqueue, KV release of finishing requests:
+        none of them depends on the token values, the trace fixes output lengths) ->
+        ``executor.wait`` for the PREVIOUS step, whose emissions are stamped with its device completion
+        time.  Decode inputs whose token is still on the device are fed there (ag_model_submit feed
+        pairs).  Scheduling decisions see the clock at planning time, one forward earlier than a
+        synchronous engine would (as any asynchronous serving scheduler)."""
+        t0 = time.perf_counter()
+        if self._origin is None:
+            self._origin = t0 - self.clock
+        self.clock = max(self.clock, self._now())
+        self._admit()
+        if not self.queue:
+            if self._inflight is not None:
+                return self.flush()
+            if self._next_arrival < len(self.trace):
+                nxt = self.trace[self._next_arrival].arrival_time
+                if nxt > self.clock:
+                    self._offset += nxt - self.clock
+                    self.clock = nxt
+            return None
+        self.queue = order_queue(self.queue, self.clock, self.stats)
+        ctx = PlanContext(self.pool, self.stats, self.profile, self.clock, set(self.long_active))
+        plan = make_plan(self.queue, ctx, self.cfg)
+        plan.check()
+        if plan.forward_size > self.executor.max_tokens or len(plan.selections) > self.executor.max_seqs:
+            raise EngineFault(f"plan of {plan.forward_size} tokens / {len(plan.selections)} sequences exceeds the "
+                              f"executor capacity ({self.executor.max_tokens}/{self.executor.max_seqs})")
+        start = self.clock
+        by_id = {e.request_id: e for e in self.queue}
+        for rid in plan.preempted:
+            e = by_id[rid]
+            tokens, table = self.pool.preempt_with_table(rid)
+            self.executor.swap_out(rid, table, tokens)
+            self.stats.observe_preemption()
+            self.metrics.requests[rid].preempt_time = start
+            e.phase = Phase.PREEMPTED
+            e.enqueue_time = start
+            e.seq = self._stamp_next()
+        if not plan.selections:
+            if plan.preempted:
+                self.metrics.iterations.append(IterationRecord(
+                    index=len(self.metrics.iterations), start=start, elapsed=0.0, forward_size=0,
+                    token_budget=plan.token_budget, num_seqs=0, num_decode=0,
+                    allocated_tokens=self.pool.allocated_tokens, preemptions=len(plan.preempted),
+                    host_pre_s=time.perf_counter() - t0))
+            if self._inflight is not None:
+                return self.flush()  # its completion may release KV / return work
+            nxt = self.trace[self._next_arrival].arrival_time if self._next_arrival < len(self.trace) else math.inf
+            jump = min(nxt, self.clock + self.stats.t_max) - self.clock
+            self._offset += max(0.0, jump)
+            self.clock += max(0.0, jump)
+            return None
+
+        # ---- allocation + packing
+        free_before = self.pool.free_blocks
+        n_sel = len(plan.selections)
+        chunk = np.empty(n_sel, np.int64)
+        before_arr = np.empty(n_sel, np.int64)
+        known: list[tuple[int, int]] = []   # (selection index, token id) decode inputs known on the host
+        feed: list[tuple[int, int]] = []    # (selection index, logit row of the step in flight)
+        tables: list[list[int]] = []
+        inflight_id = self._inflight["id"] if self._inflight is not None else -1
+        for i, sel in enumerate(plan.selections):
+            e = by_id[sel.request_id]
+            rid = sel.request_id
+            try:
+                if rid in self.pool.swapped_out:
+                    saved = self.pool.swapped_out[rid]
+                    self.pool.allocate(rid, self.pool.demand_readmit(rid))
+                    self.executor.swap_in(rid, self.pool.block_table(rid), saved)
+                    rec = self.metrics.requests[rid]
+                    if rec.preempt_time is not None:
+                        self.stats.observe_preemption_duration(start - rec.preempt_time)
+                before = self.pool.tokens_stored(rid)
+                prompt_left = has_prompt_left(e)
+                demand = (self.pool.demand_prompt_chunk(rid, sel.chunk_len) if prompt_left
+                          else self.pool.demand_tg(rid))
+                self.pool.allocate(rid, demand)
+            except (AllocationError, StateError) as exc:
+                raise EngineFault(f"plan infeasible against the pool: {exc}") from exc
+            chunk[i] = sel.chunk_len
+            before_arr[i] = before
+            if self.autoregressive and not prompt_left:
+                pend = self._pending_tok.get(rid)
+                if pend is not None and pend[0] == inflight_id:
+                    feed.append((i, pend[1]))
+                else:
+                    out = self.metrics.requests[rid].tokens_out
+                    if out and out[-1] >= 0:
+                        known.append((i, out[-1]))
+            tables.append(self.pool.block_table(rid))
+        if free_before - self.pool.free_blocks != plan.blocks_needed:
+            raise EngineFault(f"allocated {free_before - self.pool.free_blocks} blocks, plan expected "
+                              f"{plan.blocks_needed}")
+        cu = np.zeros(n_sel + 1, np.int64)
+        np.cumsum(chunk, out=cu[1:])
+        S = int(cu[-1])
+        seq_of_tok = np.repeat(np.arange(n_sel), chunk)
+        positions = (np.arange(S) - cu[seq_of_tok] + before_arr[seq_of_tok]).astype(np.int32)
+        rids_arr = np.asarray([s.request_id for s in plan.selections], np.int64)
+        token_ids = synthetic_tokens(rids_arr[seq_of_tok], positions, self.executor.vocab)
+        for i, tok in known:
+            token_ids[cu[i]] = tok
+        stride = max(len(t) for t in tables)
+        bt = np.zeros((n_sel, stride), dtype=np.int32)
+        for i, t in enumerate(tables):
+            bt[i, :len(t)] = t
+        bs = self.pool.block_size
+        slots = (bt[seq_of_tok, positions // bs] * bs + positions % bs).astype(np.int32)
+        final = np.fromiter((s.is_final_chunk for s in plan.selections), bool, n_sel)
+        logit_rows = (cu[1:][final] - 1).astype(np.int32)
+        logit_ids = [int(r) for r in rids_arr[final]]
+        batch = DeviceBatch(request_ids=[s.request_id for s in plan.selections], token_ids=token_ids,
+                            positions=positions, cu_q=cu.astype(np.int32), ctx_len=before_arr.astype(np.int32),
+                            block_table=bt, slot_mapping=slots, logit_rows=logit_rows, logit_request_ids=logit_ids)
+        if self.check:
+            self.pool.check_conservation()
+        if self.keep_history:
+            self.plans.append(plan)
+            self.tables.append({rid: list(row[:len(t)]) for rid, row, t in zip(batch.request_ids, bt, tables)})
+        fp = np.asarray([(int(cu[i]), r) for i, r in feed], np.int32).reshape(-1, 2) if feed else None
+        t_sub = time.perf_counter()
+        self.executor.submit(batch, fp)
+        sid = self._n_submitted
+        self._n_submitted += 1
+
+        # ---- optimistic state transitions (no token values needed)
+        step = {"id": sid, "start": start, "plan": plan, "logit_ids": logit_ids, "emit": [], "requeue": {},
+                "pending_prefill": [], "num_decode": 0, "host_pre_s": t_sub - t0,
+                "allocated_tokens": self.pool.allocated_tokens}
+        finished = []
+        row_of = {rid: j for j, rid in enumerate(logit_ids)}
+        for sel in plan.selections:
+            e = by_id[sel.request_id]
+            rid = sel.request_id
+            rec = self.metrics.requests[rid]
+            if e.is_offline:
+                propagate_debt(e, start - e.enqueue_time)
+            prompt = has_prompt_left(e)
+            if prompt:
+                self.stats.observe_chunk(sel.chunk_len)
+                rec.prompt_done += sel.chunk_len
+                rec.chunks.append(sel.chunk_len)
+                e.remaining_prompt_tokens -= sel.chunk_len
+                e.seq_len += sel.chunk_len
+                if e.is_long:
+                    self.long_active.add(rid)
+            else:
+                self.stats.observe_tg_step()
+                step["num_decode"] += 1
+                e.seq_len += 1
+            if not sel.is_final_chunk:
+                step["pending_prefill"].append((rid, sel.chunk_len))
+                e.phase = Phase.PROMPT_PENDING
+                e.seq = self._stamp_next()
+                continue
+            if prompt and e.is_long:
+                self.long_active.discard(rid)
+            n_emit = self._sched_emitted.get(rid, 0) + 1
+            self._sched_emitted[rid] = n_emit
+            step["emit"].append((rid, sel.chunk_len, row_of[rid]))
+            self._pending_tok[rid] = (sid, row_of[rid])
+            if n_emit >= rec.spec.output_len:
+                self.pool.release(rid)
+                finished.append(rid)
+                self._sched_emitted.pop(rid, None)
+            else:
+                e.phase = Phase.TG_READY
+                e.remaining_prompt_tokens = 0
+                e.enqueue_time = start  # provisional: set to the step's completion time when it completes
+                e.seq = self._stamp_next()
+                step["requeue"][rid] = (e, e.seq)
+        if finished:
+            gone = set(finished)
+            self.queue = [e for e in self.queue if e.request_id not in gone]
+        prev, self._inflight = self._inflight, step
+        return self._complete(prev) if prev is not None else None
+
+    def _complete(self, step: dict) -> IterationRecord:
+        """Wait for a submitted step and record its emissions at its device completion time."""
+        res = self.executor.wait()
+        end = res.end_s - self._origin + self._offset if res.end_s is not None else self._now()
+        start = max(step["start"], self._last_end)
+        end = max(end, start)
+        self._last_end = end
+        plan = step["plan"]
+        it = IterationRecord(index=len(self.metrics.iterations), start=start, elapsed=end - start,
+                             forward_size=plan.forward_size, token_budget=plan.token_budget,
+                             num_seqs=len(plan.selections), num_decode=step["num_decode"],
+                             allocated_tokens=step["allocated_tokens"], preemptions=len(plan.preempted),
+                             device_s=res.device_s, wall_s=res.wall_s, host_pre_s=step["host_pre_s"])
+        it.pending_prefill = step["pending_prefill"]
+        toks = res.token_ids.tolist()
+        for rid, chunk_len, row in step["emit"]:
+            rec = self.metrics.requests[rid]
+            spec = rec.spec
+            prev = rec.emit_times[-1] if rec.emit_times else None
+            rec.emit_times.append(end)
+            rec.generated += 1
+            rec.tokens_out.append(toks[row] if row < len(toks) else -1)
+            if rec.first_token_time is None:
+                rec.first_token_time = end
+            if spec.slo.kind is SLOKind.ONLINE:
+                it.events += 1
+                ok = (end - spec.arrival_time <= spec.slo.ttft_slo + 1e-12) if prev is None else (
+                    end - prev <= spec.slo.tbt_slo + 1e-12)
+                it.events_met += int(ok)
+                it.slo_tokens += chunk_len if ok else 0
+            else:
+                it.slo_tokens += chunk_len if end - spec.arrival_time <= spec.slo.jct_slo else 0
+            if rec.generated >= spec.output_len:
+                rec.completion_time = end
+            if self._pending_tok.get(rid, (None,))[0] == step["id"]:
+                del self._pending_tok[rid]
+            rq = step["requeue"].get(rid)
+            if rq is not None and rq[0].seq == rq[1]:
+                rq[0].enqueue_time = end  # T_w of a returned TG task starts at its emission
+        self.metrics.iterations.append(it)
+        return it
+
     def run(self, max_steps: int | None = None) -> MetricsReport:
         truncated = False
         steps = 0
@@ -529,4 +778,6 @@ class Engine:
                 break
             if self.step() is not None:
                 steps += 1
+        if self.pipeline:
+            self.flush()
         return compute_metrics(self.metrics, self.cfg.policy, truncated)

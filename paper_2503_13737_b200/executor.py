@@ -194,45 +194,128 @@ class CudaExecutor:
         dev_s = self._dev_ms.value / 1e3
         return StepResult(token_ids=out[:n].copy(), elapsed_s=dev_s, device_s=dev_s, wall_s=wall, logits=logits)
 
-    # ---------------------------------------------------------------- preemption swap (kvc.py:153-160)
-    _SWAP_STAGE_BYTES = 512 << 20  # device staging for KV swaps (a request's KV can be tens of GB)
+    # ---------------------------------------------------------------- asynchronous steps
+    def clock_ref(self) -> float:
+        """Record the device reference event and return the host time it completed at; wait() maps each
+        step's device completion onto this host clock (perf_counter seconds)."""
+        _lib.check(self.lib.ag_model_clock_ref(self.handle, torch.cuda.current_stream(self.device).cuda_stream))
+        self._ref_host = time.perf_counter()
+        return self._ref_host
 
-    def _swap_stage(self) -> tuple[torch.Tensor, int]:
-        """Persistent device staging buffer [L, 2, chunk, heads, 32, 128] and its block capacity."""
+    def submit(self, batch: DeviceBatch, feed: np.ndarray | None = None) -> None:
+        """Enqueue one forward and return (ag_model_submit); feed = int32 [n, 2] (token index, logit row of
+        the previous submitted step) for decode inputs still on the device.  At most two in flight."""
+        if getattr(self, "_ref_host", None) is None:
+            self.clock_ref()
+        st, keep = self.make_step(batch)
+        n_feed = 0 if feed is None else int(feed.shape[0])
+        fp = np.ascontiguousarray(feed, dtype=np.int32) if n_feed else None
+        logits_ptr = self.logits_buf.data_ptr() if self.logits_buf is not None else None
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        t0 = time.perf_counter()
+        _lib.check(self.lib.ag_model_submit(self.handle, C.byref(st), _np_ptr(fp) if n_feed else None, n_feed,
+                                            logits_ptr, stream))
+        wall = time.perf_counter() - t0
+        del keep
+        self.steps += 1
+        self.launches += int(self.lib.ag_model_last_launches(self.handle))
+        self.h2d_bytes += int(self.lib.ag_model_last_h2d_bytes(self.handle))
+        n = int(batch.logit_rows.shape[0])
+        self.d2h_bytes += 4 * n
+        self._pending = getattr(self, "_pending", [])
+        self._pending.append((n, wall))
+
+    def wait(self) -> StepResult:
+        """Complete the oldest submitted step: next-token ids, device time and completion time
+        (StepResult.end_s, host perf_counter seconds)."""
+        n, wall = self._pending.pop(0)
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        end_ms = C.c_double(0.0)
+        _lib.check(self.lib.ag_model_wait(self.handle, _np_ptr(out), max(n, 1), C.byref(self._dev_ms),
+                                          C.byref(end_ms)))
+        dev_s = self._dev_ms.value / 1e3
+        res = StepResult(token_ids=out[:n].copy(), elapsed_s=dev_s, device_s=dev_s, wall_s=wall)
+        res.end_s = self._ref_host + end_ms.value / 1e3
+        return res
+
+    def inflight(self) -> int:
+        return int(self.lib.ag_model_inflight(self.handle))
+
+    # ---------------------------------------------------------------- preemption swap (kvc.py:153-160)
+    _SWAP_STAGE_BYTES = 512 << 20  # per staging slot (a request's KV can be tens of GB: moved slot by slot)
+    _SWAP_SLOTS = 4
+
+    def _swap_init(self) -> None:
+        """Staging ring in HBM + a copy stream: a swap never blocks the host.  Swap-out gathers the
+        victim's blocks into a slot on the compute stream (ordered after the forwards that wrote them;
+        the freed blocks can be reallocated at once) and the copy stream drains the slot to pinned host
+        memory while later forwards run.  Swap-in copies host -> slot on the copy stream and the compute
+        stream waits for that copy only, then scatters into the newly allocated blocks."""
+        if getattr(self, "_stage", None) is not None:
+            return
         per_block = self.cfg.num_layers * 2 * self.heads_l * self.block_size * HEAD_DIM * 2
-        chunk = max(1, self._SWAP_STAGE_BYTES // per_block)
-        if getattr(self, "_stage", None) is None:
-            self._stage = torch.empty(self.cfg.num_layers, 2, chunk, self.heads_l, self.block_size, HEAD_DIM,
-                                      dtype=torch.bfloat16, device=self.device)
-        return self._stage, chunk
+        self._stage_blocks = max(1, self._SWAP_STAGE_BYTES // per_block)
+        self._stage = [torch.empty(self.cfg.num_layers, 2, self._stage_blocks, self.heads_l, self.block_size,
+                                   HEAD_DIM, dtype=torch.bfloat16, device=self.device)
+                       for _ in range(self._SWAP_SLOTS)]
+        self._slot_free = [None] * self._SWAP_SLOTS  # event after which the slot may be overwritten
+        self._slot_keep = [[] for _ in range(self._SWAP_SLOTS)]  # host tensors the slot's copies still read
+        self._next_slot = 0
+        self._copy_stream = torch.cuda.Stream(self.device)
+        self.swap_bytes = 0
+
+    def _acquire_slot(self) -> int:
+        i = self._next_slot
+        self._next_slot = (i + 1) % self._SWAP_SLOTS
+        if self._slot_free[i] is not None:
+            self._slot_free[i].synchronize()  # only blocks when every slot is still draining
+            self._slot_free[i] = None
+        self._slot_keep[i] = []
+        return i
+
+    def _ids_on_device(self, ids: list[int], keep: list) -> torch.Tensor:
+        h = torch.tensor(ids, dtype=torch.int32).pin_memory()
+        keep.append(h)  # the async H2D reads it later
+        return h.to(self.device, non_blocking=True)
 
     def _host_buffer(self, shape) -> torch.Tensor:
-        """Pinned host memory for swapped KV; pageable when the OS refuses to lock more pages."""
+        """Pinned host memory for swapped KV (torch's caching host allocator); pageable when the OS
+        refuses to lock more pages."""
         if not getattr(self, "_pin_failed", False):
             try:
                 return torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
-            except (RuntimeError, getattr(torch, "AcceleratorError", RuntimeError)):
+            except Exception:  # RuntimeError / torch.AcceleratorError: out of lockable memory
                 self._pin_failed = True
         return torch.empty(shape, dtype=torch.bfloat16)
 
     def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
-        """Preemption (reference BlockPool.preempt, kvc.py:153-160): gather the request's KV blocks
-        of every layer into the device staging buffer chunk by chunk (block_copy kernel), then copy
-        each chunk to pinned host memory."""
+        """Preemption (reference BlockPool.preempt, kvc.py:153-160): the request's KV blocks of every
+        layer go to host memory, asynchronously (see _swap_init)."""
         if not block_ids:
             return
-        stage, chunk = self._swap_stage()
+        self._swap_init()
+        comp = torch.cuda.current_stream(self.device)
         host_chunks = []
-        for c0 in range(0, len(block_ids), chunk):
-            ids = torch.tensor(block_ids[c0:c0 + chunk], dtype=torch.int32, device=self.device)
+        for c0 in range(0, len(block_ids), self._stage_blocks):
+            slot = self._acquire_slot()
+            stage = self._stage[slot]
+            keep = self._slot_keep[slot]
+            ids = self._ids_on_device(block_ids[c0:c0 + self._stage_blocks], keep)
             n = ids.numel()
             for l in range(self.cfg.num_layers):
                 for kv in range(2):
                     K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv, :n])
+            gathered = torch.cuda.Event()
+            gathered.record(comp)
             host = self._host_buffer((self.cfg.num_layers, 2, n) + tuple(stage.shape[3:]))
-            host.copy_(stage[:, :, :n], non_blocking=host.is_pinned())
-            torch.cuda.current_stream(self.device).synchronize()  # staging is reused by the next chunk
+            with torch.cuda.stream(self._copy_stream):
+                self._copy_stream.wait_event(gathered)
+                host.copy_(stage[:, :, :n], non_blocking=host.is_pinned())
+                done = torch.cuda.Event()
+                done.record(self._copy_stream)
+            self._slot_free[slot] = done
             host_chunks.append(host)
+            self.swap_bytes += host.numel() * 2
         self._swapped[request_id] = host_chunks
 
     def swap_in(self, request_id: int, block_ids: list[int], tokens: int) -> None:
@@ -244,14 +327,26 @@ class CudaExecutor:
         n_total = sum(h.shape[2] for h in host_chunks)
         if len(block_ids) < n_total:
             raise EngineFault("readmission allocated fewer blocks than were swapped out")
-        stage, _ = self._swap_stage()
+        self._swap_init()
+        comp = torch.cuda.current_stream(self.device)
         at = 0
         for host in host_chunks:
             n = host.shape[2]
-            ids = torch.tensor(block_ids[at:at + n], dtype=torch.int32, device=self.device)
-            stage[:, :, :n].copy_(host, non_blocking=host.is_pinned())
+            slot = self._acquire_slot()
+            stage = self._stage[slot]
+            keep = self._slot_keep[slot]
+            ids = self._ids_on_device(block_ids[at:at + n], keep)
+            keep.append(host)
+            with torch.cuda.stream(self._copy_stream):  # same stream as the swap-out D2H: ordered after it
+                stage[:, :, :n].copy_(host, non_blocking=host.is_pinned())
+                loaded = torch.cuda.Event()
+                loaded.record(self._copy_stream)
+            comp.wait_event(loaded)
             for l in range(self.cfg.num_layers):
                 for kv in range(2):
                     K.kv_swap_in(stage[l, kv, :n], ids, self.kv[l, kv])
-            torch.cuda.current_stream(self.device).synchronize()  # staging is reused by the next chunk
+            scattered = torch.cuda.Event()
+            scattered.record(comp)
+            self._slot_free[slot] = scattered
+            self.swap_bytes += host.numel() * 2
             at += n

@@ -88,6 +88,10 @@ class PolicyConfig:
     era: bool = True
     fcfs_budget: int | None = None    # PagedFcfs / Orca forward cap (None -> max(S_pf, 16384))
     kv_victim: str = "resident_last"  # KV-deficit victim rule: "resident_last" or the paper-literal "max_tr"
+    # admission watermark: work that holds no blocks (new prompts, readmissions) is admitted only while it
+    # leaves this fraction of the pool free for the resident requests' decode growth (vLLM's watermark);
+    # 0 = the SPEC's rule (admit up to the last free block, preempt when decodes then run out)
+    kv_watermark: float = 0.0
 
     def __post_init__(self):
         if self.policy not in POLICIES:
@@ -100,6 +104,8 @@ class PolicyConfig:
             raise ConfigError("max_concurrent_long must be >= 1")
         if self.kv_victim not in ("resident_last", "max_tr"):
             raise ConfigError("kv_victim must be 'resident_last' or 'max_tr'")
+        if not 0.0 <= self.kv_watermark < 1.0:
+            raise ConfigError("kv_watermark must be in [0, 1)")
 
 
 def token_budget(slo_min: float, profile: ModelProfile, cfg: PolicyConfig) -> int:
@@ -157,6 +163,10 @@ class PlanContext:
     long_active: set[int] = field(default_factory=set)  # long prompts with prefill started, not finished
 
 
+def watermark_blocks(pool: BlockPool, cfg: PolicyConfig) -> int:
+    return int(cfg.kv_watermark * pool.total_blocks)
+
+
 def _era_blocked(e: QueueEntry, cfg: PolicyConfig, long_active: set[int]) -> bool:
     if not (cfg.era and e.is_long and has_prompt_left(e)):
         return False
@@ -175,6 +185,7 @@ def select_requests(a_gpu: int, a_kv_tokens: int, window_src: list[QueueEntry], 
     if not window_src or a_gpu <= 0:
         return []
     pool, b = ctx.pool, ctx.pool.block_size
+    wm = watermark_blocks(pool, cfg) * b
     t1 = t_r[window_src[0].request_id]
     window = [e for e in window_src if t_r[e.request_id] <= t1 + cfg.gamma]
     a_c, a_m = a_gpu, a_kv_tokens
@@ -195,11 +206,12 @@ def select_requests(a_gpu: int, a_kv_tokens: int, window_src: list[QueueEntry], 
         for i, (pos, e) in enumerate(prompts):
             if prompt_used[i] or _era_blocked(e, cfg, long_active):
                 continue
-            c = min(e.remaining_prompt_tokens, a_c, tokens_fitting(e, a_m // b, pool))
+            room = a_m if pool.is_resident(e.request_id) else a_m - wm
+            c = min(e.remaining_prompt_tokens, a_c, tokens_fitting(e, max(0, room) // b, pool))
             if c < 1:
                 continue
             blk = step_blocks(e, c, pool)
-            if blk * b > a_m:
+            if blk * b > room:
                 continue
             key = ((a_c - c) ** 2 + (a_m - blk * b) ** 2, pos)
             if best is None or key < best[:2]:
@@ -208,6 +220,12 @@ def select_requests(a_gpu: int, a_kv_tokens: int, window_src: list[QueueEntry], 
             if not dq or blk * b > a_m:
                 continue
             pos, e = dq[0]
+            if wm and blk * b > a_m - wm and not pool.is_resident(e.request_id):
+                # a swapped-out TG task under the watermark: the next resident one of this demand competes
+                nxt = next(((p2, e2) for p2, e2 in dq if pool.is_resident(e2.request_id)), None)
+                if nxt is None:
+                    continue
+                pos, e = nxt
             key = ((a_c - 1) ** 2 + (a_m - blk * b) ** 2, pos)
             if best is None or key < best[:2]:
                 best = (key[0], pos, "t", blk, e, 1, blk)
@@ -217,7 +235,7 @@ def select_requests(a_gpu: int, a_kv_tokens: int, window_src: list[QueueEntry], 
         if kind == "p":
             prompt_used[idx] = True
         else:
-            tg_buckets[idx].popleft()
+            tg_buckets[idx].remove((best[1], e))
         taken.append((e, c, blk))
         a_c -= c
         a_m -= blk * b
@@ -269,7 +287,12 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
 
     free = pool.free_blocks
     preempted: list[int] = []
-    if members and (s_f > s_b or used > free):
+    wm = watermark_blocks(pool, cfg)
+    used_new = sum(m[2] for m in members if not pool.is_resident(m[0].request_id))
+
+    def wm_short():
+        return wm > 0 and used_new > 0 and used > free - wm
+    if members and (s_f > s_b or used > free or wm_short()):
         # repeatedly drop the member with max T_r (ties: later queue position) until B fits.  With
         # kv_victim="resident_last" a KV deficit first drops members that hold no blocks (prompts not yet
         # started, swapped-out requests awaiting readmission): admitting new work never evicts a resident
@@ -282,11 +305,14 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
         nonres = [i for i in order if not pool.is_resident(members[i][0].request_id)]
         p_all = p_nonres = 0
         dropped = set()
-        while len(dropped) < len(members) and (s_f > s_b or used > free):
+        while len(dropped) < len(members) and (s_f > s_b or used > free or wm_short()):
             kv_short = used > free
+            under_wm = not kv_short and wm_short()
             while p_nonres < len(nonres) and nonres[p_nonres] in dropped:
                 p_nonres += 1
-            if kv_short and cfg.kv_victim == "resident_last" and p_nonres < len(nonres):
+            if under_wm and s_f <= s_b:
+                i = nonres[p_nonres]  # only the admissions that cross the watermark leave B
+            elif kv_short and cfg.kv_victim == "resident_last" and p_nonres < len(nonres):
                 i = nonres[p_nonres]
             else:
                 while order[p_all] in dropped:
@@ -297,6 +323,8 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
             s_f -= c
             used -= blk
             rid = e.request_id
+            if not pool.is_resident(rid):
+                used_new -= blk
             if kv_short and pool.is_resident(rid):
                 # KV deficit: swap the victim out to free its blocks (vLLM-style preemption)
                 preempted.append(rid)

@@ -14,11 +14,11 @@ from paper_2503_13737_b200.engine import Engine  # noqa: E402
 from paper_2503_13737_b200.policies import PolicyConfig  # noqa: E402
 
 
-def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0):
+def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0, watermark=0.0, swap_cost=0.0):
     cfg = configs.config2(profile=prof, arrival_rate=rate, num_requests=n_req, seed=seed)
     trace = wl.generate_trace(cfg.trace)
-    eng = Engine(trace, prof, PolicyConfig(policy=policy), clock="virtual",
-                 kv_blocks=prof.kvc_capacity_tokens // 32)
+    eng = Engine(trace, prof, PolicyConfig(policy=policy, kv_watermark=watermark), clock="virtual",
+                 kv_blocks=prof.kvc_capacity_tokens // 32, per_token_swap_cost_s=swap_cost)
     w0 = time.time()
     while not eng.done() and eng.clock < horizon:
         eng.step()
@@ -30,7 +30,7 @@ def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0):
     slo = sum(it.slo_tokens for it in its)
     dec = sum(it.num_decode for it in its)
     live = len(eng.queue)
-    return {"rate": rate, "policy": policy, "iters": len(its), "ms_per_iter": 1e3 * span / max(1, len(its)),
+    return {"rate": rate, "policy": policy, "wm": watermark, "iters": len(its), "ms_per_iter": 1e3 * span / max(1, len(its)),
             "attain": met / ev if ev else None, "fwd_tok_s": toks / span, "slo_tok_s": slo / span,
             "decode_tok_s": dec / span, "preempt": sum(it.preemptions for it in its),
             "S_f_p50": float(np.median([it.forward_size for it in its])) if its else 0,
@@ -45,10 +45,14 @@ if __name__ == "__main__":
     ap.add_argument("--horizon", type=float, default=300)
     ap.add_argument("--t0", type=float, default=120)
     ap.add_argument("--profile", default=None)
+    ap.add_argument("--watermarks", default="0")
+    ap.add_argument("--swap-cost", type=float, default=819200 / 25e9, help="s per swapped token (PCIe)")
     a = ap.parse_args()
     prof = cm.load_profile(a.profile) if a.profile else cm.ModelProfile(
         hidden_size=5120, num_layers=40, pivot_forward_size=1536, pivot_time_s=0.033, fixed_overhead_s=0.0045,
         kvc_capacity_tokens=186720, kv_read_s_per_token=1.3e-7, attn_s_per_pair=1.2e-9)
     for pol in a.policies.split(","):
         for r in a.rates.split(","):
-            print(json.dumps(run(float(r), pol, a.horizon, a.t0, prof)), flush=True)
+            for wm in a.watermarks.split(","):
+                print(json.dumps(run(float(r), pol, a.horizon, a.t0, prof, watermark=float(wm),
+                                     swap_cost=a.swap_cost)), flush=True)

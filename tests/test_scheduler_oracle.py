@@ -9,11 +9,12 @@ from paper_2503_13737_b200.engine import Engine
 from paper_2503_13737_b200.policies import PolicyConfig
 
 
-def _compare(trace, prof, kv_blocks=None, max_steps=None, kv_victim="resident_last"):
-    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim), kv_blocks=kv_blocks, check_invariants=True)
+def _compare(trace, prof, kv_blocks=None, max_steps=None, kv_victim="resident_last", kv_watermark=0.0):
+    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark), kv_blocks=kv_blocks,
+                 check_invariants=True)
     eng.keep_history = True
     eng.run(max_steps=max_steps)
-    orc = OracleScheduler(trace, prof, kv_blocks=kv_blocks, kv_victim=kv_victim)
+    orc = OracleScheduler(trace, prof, kv_blocks=kv_blocks, kv_victim=kv_victim, kv_watermark=kv_watermark)
     log = orc.run(max_steps=max_steps)
     assert len(log) == len(eng.plans)
     for i, (plan, tables, ref) in enumerate(zip(eng.plans, eng.tables, log)):
@@ -31,19 +32,20 @@ def test_config1_decisions_match_oracle():
     assert n > 1000
 
 
-@pytest.mark.parametrize("kv_victim", ["resident_last", "max_tr"])
-def test_kv_pressure_with_preemption_matches_oracle(kv_victim):
+@pytest.mark.parametrize("kv_victim,kv_watermark", [("resident_last", 0.0), ("max_tr", 0.0),
+                                                    ("resident_last", 0.1)])
+def test_kv_pressure_with_preemption_matches_oracle(kv_victim, kv_watermark):
     """Small KV pool (paper-like capped regime): urgency, preemption (swap-out) and readmission, under
-    both KV-deficit victim rules."""
+    both KV-deficit victim rules and with an admission watermark."""
     c = configs.config1()
     prof = cm.ModelProfile(hidden_size=256, num_layers=2, pivot_forward_size=256, pivot_time_s=0.002,
                            fixed_overhead_s=0.002, kvc_capacity_tokens=48 * 32)
     trace = wl.generate_trace(wl.TraceConfig(**{**c.trace.__dict__, "num_requests": 40, "profile": prof,
                                                 "long_fraction": 0.0,
                                                 "output_len_dist": wl.LengthDist("uniform", 100, 400)}))
-    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim), kv_blocks=48)
+    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark), kv_blocks=48)
     assert eng.run().preemptions > 5  # the scenario really exercises preemption
-    n = _compare(trace, prof, kv_blocks=48, kv_victim=kv_victim)
+    n = _compare(trace, prof, kv_blocks=48, kv_victim=kv_victim, kv_watermark=kv_watermark)
     assert n > 1000
 
 

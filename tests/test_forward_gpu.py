@@ -226,25 +226,34 @@ def test_175b_shape_two_layers_vs_oracle():
     tally.check("175B-shape 2 layers")
 
 
-def test_executor_swap_roundtrip_chunked():
+@pytest.mark.parametrize("per_chunk", [3, 1])
+def test_executor_swap_roundtrip_chunked(per_chunk):
     """Preemption swap through the executor (kvc.py:153-160 preempt / demand_readmit): a request's
-    blocks of every layer go to host memory through a bounded device staging buffer in several
-    chunks, and come back bit-exactly into different physical blocks."""
+    blocks of every layer go to host memory through the HBM staging ring in several chunks (1 block per
+    chunk: 8 chunks cycle the 4-slot ring twice) without host synchronisation, the freed blocks are
+    overwritten at once on the compute stream, and everything comes back bit-exactly into different
+    physical blocks -- also for a second request swapped while the first is still on the host."""
     from paper_2503_13737_b200.executor import CudaExecutor
     cfg = M.tiny()
     w = M.init_weights(cfg, seed=0, init="test")
     dev = CudaExecutor(cfg, 64, max_tokens=256, max_seqs=8, weights=w, autotune=False)
-    dev._SWAP_STAGE_BYTES = 3 * cfg.num_layers * 2 * dev.heads_l * 32 * 128 * 2  # 3 blocks per chunk
+    dev._SWAP_STAGE_BYTES = per_chunk * cfg.num_layers * 2 * dev.heads_l * 32 * 128 * 2
     g = torch.Generator(device="cuda").manual_seed(3)
     dev.kv.copy_(torch.randn(dev.kv.shape, generator=g, device="cuda").to(torch.bfloat16))
     src = [5, 9, 2, 40, 41, 17, 63, 0]
+    src2 = [30, 31, 32]
     before = dev.kv[:, :, src].clone()
+    before2 = dev.kv[:, :, src2].clone()
     dev.swap_out(7, src, 8 * 32)
-    assert len(dev._swapped[7]) == 3                 # ceil(8 / 3) chunks
-    dev.kv[:, :, src] = 0
+    assert len(dev._swapped[7]) == -(-8 // per_chunk)
+    dev.kv[:, :, src] = 0                             # reuse of the freed blocks, stream-ordered
+    dev.swap_out(8, src2, 3 * 32)
+    dev.kv[:, :, src2] = 1
     dst = [10, 11, 12, 13, 14, 15, 16, 18]
     dev.swap_in(7, dst, 8 * 32)
+    dev.swap_in(8, [5, 9, 2], 3 * 32)
     assert torch.equal(dev.kv[:, :, dst], before)
+    assert torch.equal(dev.kv[:, :, [5, 9, 2]], before2)
 
 
 def test_forward_at_capacity_limits():

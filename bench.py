@@ -163,7 +163,7 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2503_13737_b200 import tp as TP
     from paper_2503_13737_b200 import workload
-    from paper_2503_13737_b200.cost_model import ModelProfile, forward_flops
+    from paper_2503_13737_b200.cost_model import ModelProfile, forward_bytes, forward_flops
     from paper_2503_13737_b200.engine import Engine
     from paper_2503_13737_b200.executor import CudaExecutor
     from paper_2503_13737_b200.policies import PolicyConfig
@@ -339,6 +339,11 @@ def run_ours(args):
     K = args.steps
     H, F, L, V = mcfg.hidden, mcfg.ffn, mcfg.num_layers, mcfg.vocab
     flops = sum(forward_flops(b.seq_shapes(), len(b.logit_rows), H, F, L, V, world) for b in batches)
+    hbm_bytes = sum(forward_bytes(b.seq_shapes(), H, F, L, V, world) for b in batches)
+    # per forward: max(FLOPs / tensor peak, compulsory bytes / HBM peak), summed -- the time the step
+    # would take at the roofline (weights + K/V read once)
+    roof_s = sum(max(forward_flops(b.seq_shapes(), len(b.logit_rows), H, F, L, V, world) / (peaks["tensor_sustained"] * 1e12),
+                     forward_bytes(b.seq_shapes(), H, F, L, V, world) / (peaks["hbm"] * 1e9)) for b in batches)
     gemm_cls = ("qkv_gemm", "out_gemm", "fc1_gemm", "fc2_gemm", "lmhead_gemm")
     g_ms = sum(prof_k[c]["ms"] for c in gemm_cls)
     g_fl = sum(prof_k[c]["flops"] for c in gemm_cls)
@@ -423,7 +428,10 @@ def run_ours(args):
         "gpu_launches": launches_timed,
         "roofline": roof_dominant,
         "roofline_by_kernel": roof_all,
-        "forward_roofline": {"achieved_tflops": flops / dev_s / 1e12 if dev_s else 0.0,
+        "forward_roofline": {"roofline_time_frac": roof_s / dev_s if dev_s else None,
+                             "achieved_hbm_gbs": hbm_bytes / dev_s / 1e9 if dev_s else 0.0,
+                             "hbm_frac": hbm_bytes / dev_s / 1e9 / peaks["hbm"] if dev_s else None,
+                             "achieved_tflops": flops / dev_s / 1e12 if dev_s else 0.0,
                              "frac_of_sustained": flops / dev_s / 1e12 / peaks["tensor_sustained"] if dev_s else None},
         "attention": {"ms": attn["ms"], "tflops": attn["flops"] / (attn["ms"] / 1e3) / 1e12 if attn["ms"] else 0.0,
                       "gbs": attn["bytes"] / (attn["ms"] / 1e3) / 1e9 if attn["ms"] else 0.0},

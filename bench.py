@@ -58,6 +58,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kv-watermark", type=float, default=0.1,
                     help="AccelGen admission watermark (fraction of the KV pool kept for decode growth)")
+    ap.add_argument("--spec-policy", action="store_true",
+                    help="the SPEC restatement of AccelGen only: no watermark, no TG retention, SPEC budget rule")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="synchronous engine (plan, forward, emit in turn) instead of planning step k+1 during k")
     return ap.parse_args()
@@ -231,8 +233,9 @@ def run_ours(args):
     trace = workload.generate_trace(cfg.trace)
     executor = TP.TPLeader(ex, group) if world > 1 else ex
     pipeline = world == 1 and not args.no_pipeline  # TP followers mirror synchronous steps
-    eng = Engine(trace, prof, PolicyConfig(policy=args.policy, kv_watermark=args.kv_watermark), executor,
-                 clock="wall", kv_blocks=num_blocks, pipeline=pipeline)
+    pcfg = PolicyConfig(policy=args.policy) if args.spec_policy else PolicyConfig(
+        policy=args.policy, kv_watermark=args.kv_watermark, retain_tg=True, budget_live_only=True)
+    eng = Engine(trace, prof, pcfg, executor, clock="wall", kv_blocks=num_blocks, pipeline=pipeline)
 
     def serve_until(t_end):
         its = []
@@ -411,7 +414,9 @@ def run_ours(args):
                    "kv_pool_tokens": num_blocks * 32, "step": f"{args.window_s:g} s window of serving",
                    "ramp_s": ramp_s, "forward_tokens_per_step": tokens / K,
                    "l2": "inputs larger than L2 (26 GB of weights + K/V per forward)", "clock": "wall (live)",
-                   "pipelined_host": pipeline, "kv_watermark": args.kv_watermark},
+                   "pipelined_host": pipeline,
+                   "policy_refinements": None if args.spec_policy else
+                   {"kv_watermark": args.kv_watermark, "retain_tg": True, "budget_live_only": True}},
         "iter_slo_attainment": met / events if events else None,
         "steady_state": {"ramp_wall_s": ramp_wall, "live_requests": live0, "kv_occupancy": kv0,
                          "forwards_per_window": len(recs) / K,

@@ -99,12 +99,14 @@ class OracleScheduler:
     """Virtual-clock AccelGen simulation over a trace; records every plan."""
 
     def __init__(self, trace, profile, *, gamma=0.75, max_long=1, slack=0.1, kv_blocks=None, era=True,
-                 kv_victim="resident_last", kv_watermark=0.0):
+                 kv_victim="resident_last", kv_watermark=0.0, retain_tg=False, budget_live_only=False):
         self.trace = sorted(trace, key=lambda r: (r.arrival_time, r.id))
         self.p = profile
         self.gamma, self.max_long, self.slack, self.era = gamma, max_long, slack, era
         self.kv_victim = kv_victim
         self.kv_watermark = kv_watermark
+        self.retain_tg = retain_tg
+        self.budget_live_only = budget_live_only
         self.pool = Pool(kv_blocks if kv_blocks is not None else profile.kvc_capacity_tokens // 32)
         self.t_max = profile.fixed_overhead_s + profile.pivot_time_s * profile.pivot_forward_size / profile.pivot_forward_size
         self.lc = float(profile.pivot_forward_size)
@@ -162,7 +164,8 @@ class OracleScheduler:
         tr = {r.rid: self.t_r(r, now) for r in q}
         pos = {r.rid: i for i, r in enumerate(q)}
         urgent = [r for r in q if tr[r.rid] <= self.t_max * (1.0 + self.slack)]
-        online = [self.slo(r) for r in urgent + q[:1] if r.online]
+        online = [self.slo(r) for r in urgent + q[:1]
+                  if r.online and (not self.budget_live_only or now - r.enqueue <= self.slo(r))]
         s_b = self.budget(min(online)) if online else self.p.pivot_forward_size
         active = set(self.long_active)
         new_here = set()
@@ -248,6 +251,20 @@ class OracleScheduler:
                 a_m -= blk * pool.b
                 if r.long and self.prompt_left(r):
                     active.add(r.rid)
+        if self.retain_tg:  # every resident TG task not in B joins it while budget and blocks allow
+            a_c = s_b - sum(c for _, c, _ in chosen)
+            a_blk = free - sum(blk for _, _, blk in chosen)
+            taken = {r.rid for r, _, _ in chosen}
+            for r in rest:
+                if a_c < 1:
+                    break
+                if r.rid in taken or self.prompt_left(r) or r.rid not in pool.tables:
+                    continue
+                blk = pool.need(r, 1)
+                if blk <= a_blk:
+                    chosen.append((r, 1, blk))
+                    a_c -= 1
+                    a_blk -= blk
         return s_b, chosen, preempted, deferred
 
     # ---- engine step (SPEC.md:481-489 with the pinned decisions)

@@ -92,6 +92,15 @@ class PolicyConfig:
     # leaves this fraction of the pool free for the resident requests' decode growth (vLLM's watermark);
     # 0 = the SPEC's rule (admit up to the last free block, preempt when decodes then run out)
     kv_watermark: float = 0.0
+    # PAPER §4.4 "the previous TG requests should be retained in the batch as much as possible": after
+    # Algorithms 1-2, every resident TG task not yet in B joins it (queue order) while budget and free
+    # blocks allow.  Off = the SPEC's restatement (TG tasks join only when urgent or in the gamma-window)
+    retain_tg: bool = False
+    # budget from live deadlines only: an entry whose current iteration deadline has already passed
+    # (T_w > its iteration SLO) no longer constrains S_b -- shrinking the forward cannot make a missed
+    # deadline, it only starves everyone else (with B200 TTFT SLOs of ~5-15 ms, below one decode-carrying
+    # step, the SPEC rule holds S_b near 200 tokens and chunks resident prompts one token per step)
+    budget_live_only: bool = False
 
     def __post_init__(self):
         if self.policy not in POLICIES:
@@ -173,8 +182,10 @@ def _era_blocked(e: QueueEntry, cfg: PolicyConfig, long_active: set[int]) -> boo
     return e.request_id not in long_active and len(long_active) >= cfg.max_concurrent_long
 
 
-def _slo_min(entries) -> float | None:
-    vals = [iteration_slo(e) for e in entries if e.request.slo.kind is SLOKind.ONLINE]
+def _slo_min(entries, now: float | None = None) -> float | None:
+    """Smallest online iteration SLO; with `now`, only over entries whose deadline is still ahead."""
+    vals = [iteration_slo(e) for e in entries if e.request.slo.kind is SLOKind.ONLINE
+            and (now is None or now - e.enqueue_time <= iteration_slo(e))]
     return min(vals) if vals else None
 
 
@@ -252,7 +263,7 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
     t_r = {e.request_id: remaining_time(e, ctx.now, stats) for e in queue}
     position = {e.request_id: i for i, e in enumerate(queue)}
     urgent = [e for e in queue if is_urgent(t_r[e.request_id], stats, cfg.urgency_slack)]
-    slo_min = _slo_min(urgent + [queue[0]])
+    slo_min = _slo_min(urgent + [queue[0]], ctx.now if cfg.budget_live_only else None)
     if slo_min is None:
         cap = profile.pivot_forward_size if cfg.budget_cap is None else cfg.budget_cap
         s_b, slo_min = cap, 0.0
@@ -341,6 +352,21 @@ def accelgen_plan(queue: list[QueueEntry], ctx: PlanContext, cfg: PolicyConfig) 
     skip = {e.request_id for e in urgent} | set(preempted) | set(deferred)
     rest = [e for e in queue if e.request_id not in skip]
     chosen += select_requests(s_b - s_f, (free - used) * pool.block_size, rest, t_r, ctx, cfg, long_active)
+    if cfg.retain_tg:
+        a_c = s_b - sum(c for _, c, _ in chosen)
+        a_blk = free - sum(blk for _, _, blk in chosen)
+        taken = {e.request_id for e, _, _ in chosen}
+        for e in rest:
+            if a_c < 1:
+                break
+            if e.request_id in taken or has_prompt_left(e) or not pool.is_resident(e.request_id):
+                continue
+            blk = step_blocks(e, 1, pool)
+            if blk > a_blk:
+                continue
+            chosen.append((e, 1, blk))
+            a_c -= 1
+            a_blk -= blk
 
     plan = BatchPlan(token_budget=s_b, preempted=preempted, slo_min=slo_min, deferred=deferred)
     for e, c, blk in chosen:

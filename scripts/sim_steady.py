@@ -14,10 +14,10 @@ from paper_2503_13737_b200.engine import Engine  # noqa: E402
 from paper_2503_13737_b200.policies import PolicyConfig  # noqa: E402
 
 
-def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0, watermark=0.0, swap_cost=0.0):
+def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0, watermark=0.0, swap_cost=0.0, retain_tg=False, live_only=False):
     cfg = configs.config2(profile=prof, arrival_rate=rate, num_requests=n_req, seed=seed)
     trace = wl.generate_trace(cfg.trace)
-    eng = Engine(trace, prof, PolicyConfig(policy=policy, kv_watermark=watermark), clock="virtual",
+    eng = Engine(trace, prof, PolicyConfig(policy=policy, kv_watermark=watermark, retain_tg=retain_tg, budget_live_only=live_only), clock="virtual",
                  kv_blocks=prof.kvc_capacity_tokens // 32, per_token_swap_cost_s=swap_cost)
     w0 = time.time()
     while not eng.done() and eng.clock < horizon:
@@ -30,7 +30,7 @@ def run(rate, policy, horizon, t0, prof, n_req=6000, seed=0, watermark=0.0, swap
     slo = sum(it.slo_tokens for it in its)
     dec = sum(it.num_decode for it in its)
     live = len(eng.queue)
-    return {"rate": rate, "policy": policy, "wm": watermark, "iters": len(its), "ms_per_iter": 1e3 * span / max(1, len(its)),
+    return {"rate": rate, "policy": policy, "wm": watermark, "retain_tg": retain_tg, "live_only": live_only, "iters": len(its), "ms_per_iter": 1e3 * span / max(1, len(its)),
             "attain": met / ev if ev else None, "fwd_tok_s": toks / span, "slo_tok_s": slo / span,
             "decode_tok_s": dec / span, "preempt": sum(it.preemptions for it in its),
             "S_f_p50": float(np.median([it.forward_size for it in its])) if its else 0,
@@ -46,6 +46,8 @@ if __name__ == "__main__":
     ap.add_argument("--t0", type=float, default=120)
     ap.add_argument("--profile", default=None)
     ap.add_argument("--watermarks", default="0")
+    ap.add_argument("--retain-tg", action="store_true")
+    ap.add_argument("--live-only", action="store_true")
     ap.add_argument("--swap-cost", type=float, default=819200 / 25e9, help="s per swapped token (PCIe)")
     a = ap.parse_args()
     prof = cm.load_profile(a.profile) if a.profile else cm.ModelProfile(
@@ -55,4 +57,4 @@ if __name__ == "__main__":
         for r in a.rates.split(","):
             for wm in a.watermarks.split(","):
                 print(json.dumps(run(float(r), pol, a.horizon, a.t0, prof, watermark=float(wm),
-                                     swap_cost=a.swap_cost)), flush=True)
+                                     swap_cost=a.swap_cost, retain_tg=a.retain_tg, live_only=a.live_only)), flush=True)

@@ -221,7 +221,7 @@ def test_mixed_attention(K, seqs, heads):
     ([(0, 1000)], 40),
     # chunk whose causal end is inside the first KV tile of a split
     ([(12000, 130), (7, 3)], 2),
-    # many more (tile item, head) units than SMs: persistent tile CTAs run several units each
+    # many more (tile item, head) units than SMs: several waves of tile CTAs interleaved with the rows
     ([(0, 512)] * 6 + [(3000, 300), (9000, 1), (0, 40)], 24),
 ])
 def test_mixed_attention_boundaries(K, seqs, heads):

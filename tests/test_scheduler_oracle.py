@@ -9,12 +9,15 @@ from paper_2503_13737_b200.engine import Engine
 from paper_2503_13737_b200.policies import PolicyConfig
 
 
-def _compare(trace, prof, kv_blocks=None, max_steps=None, kv_victim="resident_last", kv_watermark=0.0):
-    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark), kv_blocks=kv_blocks,
-                 check_invariants=True)
+def _compare(trace, prof, kv_blocks=None, max_steps=None, kv_victim="resident_last", kv_watermark=0.0,
+             retain_tg=False, live_only=False):
+    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark, retain_tg=retain_tg,
+                                           budget_live_only=live_only),
+                 kv_blocks=kv_blocks, check_invariants=True)
     eng.keep_history = True
     eng.run(max_steps=max_steps)
-    orc = OracleScheduler(trace, prof, kv_blocks=kv_blocks, kv_victim=kv_victim, kv_watermark=kv_watermark)
+    orc = OracleScheduler(trace, prof, kv_blocks=kv_blocks, kv_victim=kv_victim, kv_watermark=kv_watermark,
+                          retain_tg=retain_tg, budget_live_only=live_only)
     log = orc.run(max_steps=max_steps)
     assert len(log) == len(eng.plans)
     for i, (plan, tables, ref) in enumerate(zip(eng.plans, eng.tables, log)):
@@ -32,9 +35,10 @@ def test_config1_decisions_match_oracle():
     assert n > 1000
 
 
-@pytest.mark.parametrize("kv_victim,kv_watermark", [("resident_last", 0.0), ("max_tr", 0.0),
-                                                    ("resident_last", 0.1)])
-def test_kv_pressure_with_preemption_matches_oracle(kv_victim, kv_watermark):
+@pytest.mark.parametrize("kv_victim,kv_watermark,retain_tg", [("resident_last", 0.0, False), ("max_tr", 0.0, False),
+                                                              ("resident_last", 0.1, False),
+                                                              ("resident_last", 0.1, True)])
+def test_kv_pressure_with_preemption_matches_oracle(kv_victim, kv_watermark, retain_tg):
     """Small KV pool (paper-like capped regime): urgency, preemption (swap-out) and readmission, under
     both KV-deficit victim rules and with an admission watermark."""
     c = configs.config1()
@@ -43,9 +47,10 @@ def test_kv_pressure_with_preemption_matches_oracle(kv_victim, kv_watermark):
     trace = wl.generate_trace(wl.TraceConfig(**{**c.trace.__dict__, "num_requests": 40, "profile": prof,
                                                 "long_fraction": 0.0,
                                                 "output_len_dist": wl.LengthDist("uniform", 100, 400)}))
-    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark), kv_blocks=48)
+    eng = Engine(trace, prof, PolicyConfig(kv_victim=kv_victim, kv_watermark=kv_watermark, retain_tg=retain_tg),
+                 kv_blocks=48)
     assert eng.run().preemptions > 5  # the scenario really exercises preemption
-    n = _compare(trace, prof, kv_blocks=48, kv_victim=kv_victim, kv_watermark=kv_watermark)
+    n = _compare(trace, prof, kv_blocks=48, kv_victim=kv_victim, kv_watermark=kv_watermark, retain_tg=retain_tg)
     assert n > 1000
 
 
@@ -81,3 +86,14 @@ def test_batch_time_reduces_to_reference_linear_model():
     ext = cm.ModelProfile(**{**prof.__dict__, "kv_read_s_per_token": 1e-7, "attn_s_per_pair": 1e-9})
     assert cm.batch_features([(1, 2048), (512, 0)]) == (2049 + 512, 2049 + 512 * 513 // 2)
     assert cm.batch_time(768, 1000, 10, ext) == cm.iteration_time(768, prof) + 1e-7 * 1000 + 1e-9 * 10
+
+
+def test_retain_tg_matches_oracle_b200_profile():
+    """PAPER §4.4 TG retention on a B200-like profile with a large pool (decodes join B every step)."""
+    prof = cm.ModelProfile(hidden_size=5120, num_layers=40, pivot_forward_size=1536, pivot_time_s=0.0367,
+                           fixed_overhead_s=0.0037, kvc_capacity_tokens=40000, kv_read_s_per_token=1.4e-7,
+                           attn_s_per_pair=7e-10)
+    cfg = configs.config2(profile=prof, num_requests=150, arrival_rate=6.0).trace
+    trace = wl.generate_trace(cfg)
+    _compare(trace, prof, max_steps=1500, kv_watermark=0.1, retain_tg=True)
+    _compare(trace, prof, max_steps=1500, kv_watermark=0.1, retain_tg=True, live_only=True)

@@ -32,7 +32,31 @@ def case(name: str):
             [(0, 956, 1), (1, 301, 1), (2, 34, 1), (3, 90, 1)] + [(rid, p + 1, 1) for rid, p in dec],
         ]
         return cfg, 11, 1024, steps
+    if name == "175b2l":  # config 5 shape: OPT-175B (H=12288, 96 heads, FFN 49152), 2 of 96 layers
+        cfg = M.OPTConfig("opt-175b-2l", hidden=12288, num_layers=2, num_heads=96, ffn=49152, max_positions=4096)
+        dec = [(10 + i, 30 + 11 * i) for i in range(16)]
+        steps = [
+            [(0, 0, 900), (1, 0, 257)] + [(rid, 0, p) for rid, p in dec],
+            [(0, 900, 300), (1, 257, 1), (2, 0, 64)] + [(rid, p, 1) for rid, p in dec],
+            [(0, 1200, 1), (1, 258, 1), (2, 64, 1)] + [(rid, p + 1, 1) for rid, p in dec],
+        ]
+        return cfg, 13, 1024, steps
+    if name == "13b100k":  # config 4 regime: a 100k-token prompt chunked (8 chunks), a decode, + 2 short
+        P, C = 100_000, 12_500
+        cfg = M.OPTConfig("opt-13b-2l-100k", hidden=5120, num_layers=2, num_heads=40, ffn=20480, max_positions=P + 64)
+        steps = [[(0, s, C)] for s in range(0, P - C, C)]
+        steps.append([(0, P - C, C), (1, 0, 200)])
+        steps.append([(0, P, 1), (1, 200, 1), (2, 0, 37)])
+        return cfg, 17, P // 32 + 64, steps
     raise ValueError(name)
+
+
+def checked_steps(name: str) -> set[int]:
+    """Indices of the steps whose logits the test compares (all, except the long prefill chunks)."""
+    cfg, _, _, steps = case(name)
+    if name == "13b100k":
+        return {len(steps) - 3, len(steps) - 2, len(steps) - 1}
+    return set(range(len(steps)))
 
 
 def main():
@@ -56,8 +80,9 @@ def main():
     cfg, seed, blocks, steps = case(a.case)
     w = M.init_weights(cfg, seed, device="cuda", tp_rank=a.rank, tp_size=a.world, init="test")
     hc = HostCollective(dist.group.WORLD, a.world)
-    ex = CudaExecutor(cfg, blocks, max_tokens=4096, max_seqs=64, weights=w, tp_rank=a.rank, tp_size=a.world,
-                      parity_logits=True, autotune=False, host_collective=hc)
+    ex = CudaExecutor(cfg, blocks, max_tokens=max(4096, max(sum(n for *_, n in s) for s in steps)), max_seqs=64,
+                      weights=w, tp_rank=a.rank, tp_size=a.world, parity_logits=True, autotune=False,
+                      host_collective=hc, max_blocks_per_seq=(cfg.pos_rows + 31) // 32)
     pool = BlockPool(blocks)
     res = []
     for segs in steps:

@@ -62,7 +62,10 @@ def _run_one(trace, profile, policy: str, executor_kind: str, horizon: float, kv
                                                                              for r in trace) + 64)
         blocks = kv_blocks or max(1, profile.kvc_capacity_tokens // 32)
         ex = CudaExecutor(mcfg, blocks, max_tokens=max(profile.pivot_forward_size, 16384), max_seqs=2048)
-        eng = Engine(trace, profile, pc, ex, clock="device", kv_blocks=blocks, horizon_s=horizon)
+        try:
+            return Engine(trace, profile, pc, ex, clock="device", kv_blocks=blocks, horizon_s=horizon).run()
+        finally:
+            ex.close()  # weights + a KV pool sized to the profile: give the HBM back before the next policy
     return eng.run()
 
 

@@ -40,6 +40,10 @@ def test_tp_sharded_forward_vs_unsharded_oracle(tp, name, tmp_path):
     from paper_2503_13737_b200 import model as M
     from paper_2503_13737_b200.kvc import BlockPool
 
+    # the workers share this GPU: hand back what earlier tests in this process left in torch's cache
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     port = _free_port()
     procs = [subprocess.Popen([sys.executable, str(HERE / "tp_gpu_worker.py"), "--rank", str(r), "--world", str(tp),
                                "--port", str(port), "--case", name, "--out", str(tmp_path / f"rank{r}.pt")])

@@ -206,6 +206,7 @@ def run_ours(args):
                       max_blocks_per_seq=(mcfg.pos_rows + 31) // 32, tp_rank=rank, tp_size=world, seed=0,
                       init="opt", nccl_uid=uid, host_collective=host_coll)
     torch.cuda.synchronize()
+    free_after_setup = torch.cuda.mem_get_info()[0]
 
     if rank != 0:
         # followers: mirror rank 0's steps; report own device time for the max-over-ranks
@@ -424,6 +425,8 @@ def run_ours(args):
                          "prompts_credit_unresolved": unresolved},
         "preemptions_in_window": sum(r.preemptions for r in recs),
         "swap_gb_total": getattr(ex, "swap_bytes", 0) / 1e9,
+        "hbm_gb": {"kv_pool": num_blocks * 32 * kv_tok_bytes / 1e9, "free_after_setup": free_after_setup / 1e9,
+                   "free_at_end": torch.cuda.mem_get_info()[0] / 1e9},
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,
         "forward_size_pct": {q: int(np.percentile([r.forward_size for r in recs], q)) for q in (10, 50, 90, 99)},
         "token_events": events,

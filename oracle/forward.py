@@ -148,7 +148,7 @@ class OracleOPT:
     (full model, tp_size=1) or one TP shard when tp_size > 1 (then ``allreduce`` sums partials)."""
 
     def __init__(self, cfg, weights, num_blocks, block_size=32, tp_rank=0, tp_size=1, allreduce=None,
-                 device="cpu", acc=torch.float32):
+                 device="cpu", acc=torch.float32, tp_emulate=1):
         self.cfg = cfg
         self.acc = acc
         self.dev = torch.device(device)
@@ -156,6 +156,10 @@ class OracleOPT:
         self.block_size = block_size
         self.tp_rank, self.tp_size = tp_rank, tp_size
         self.allreduce = allreduce
+        # tp_emulate=t (unsharded weights): out-proj / FC2 as t column-shard partials, each rounded to bf16
+        # as the sharded GEMM epilogue stores it, summed in fp32 and rounded once (the all-reduce), then
+        # + bias + residual (the LayerNorm that follows the reduce) -- the TP=t device's rounding points
+        self.tp_emulate = tp_emulate if tp_size == 1 else 1
         heads_l = cfg.num_heads // tp_size
         self.heads_l = heads_l
         pool_dtype = torch.bfloat16 if ROUND_BF16 else torch.float32
@@ -168,6 +172,16 @@ class OracleOPT:
         if self.tp_size == 1:
             return partial
         return self.allreduce(partial)
+
+    def _row_parallel(self, a, w):
+        """a @ w.T computed the way tp_emulate ranks do (Megatron row split of w by input columns)."""
+        t = self.tp_emulate
+        k = w.shape[1] // t
+        parts = [rb(a[:, r * k:(r + 1) * k] @ f32(w[:, r * k:(r + 1) * k]).T) for r in range(t)]
+        total = parts[0]
+        for p in parts[1:]:
+            total = total + p
+        return rb(total)
 
     def forward(self, st: StepInputs):
         global DEVICE, ACC
@@ -197,17 +211,21 @@ class OracleOPT:
             kv_append(k, v, st.slot_mapping, self.k_pools[l], self.v_pools[l], self.block_size)
             a = rb(paged_attention(q, self.k_pools[l], self.v_pools[l], st.block_table, st.cu_q, st.ctx_len,
                                    self.block_size))
-            if self.tp_size == 1:
+            if self.tp_emulate > 1:
+                x = rb(x + (self._row_parallel(a, L["out_w"]) + f32(L["out_b"])))
+            elif self.tp_size == 1:
                 x = rb(a @ f32(L["out_w"]).T + f32(L["out_b"]) + x)
             else:
-                part = self._reduce(rb(a @ f32(L["out_w"]).T))
+                part = rb(self._reduce(rb(a @ f32(L["out_w"]).T)))  # bf16 all-reduce output
                 x = rb(x + (part + f32(L["out_b"])))
             h = layernorm(x, L["ln2_g"], L["ln2_b"], cfg.ln_eps)
             f = rb(torch.relu(h @ f32(L["fc1_w"]).T + f32(L["fc1_b"])))
-            if self.tp_size == 1:
+            if self.tp_emulate > 1:
+                x = rb(x + (self._row_parallel(f, L["fc2_w"]) + f32(L["fc2_b"])))
+            elif self.tp_size == 1:
                 x = rb(f @ f32(L["fc2_w"]).T + f32(L["fc2_b"]) + x)
             else:
-                part = self._reduce(rb(f @ f32(L["fc2_w"]).T))
+                part = rb(self._reduce(rb(f @ f32(L["fc2_w"]).T)))
                 x = rb(x + (part + f32(L["fc2_b"])))
         rows = st.logit_rows.long()
         hl = layernorm(x[rows], w["final_g"], w["final_b"], cfg.ln_eps)

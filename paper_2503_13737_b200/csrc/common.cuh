@@ -307,9 +307,21 @@ inline bool pdl_enabled(int cls) {
   return (mask & cls) != 0;
 }
 
+// AG_ABLATE=<bits> (same classes): skip those launches entirely.  Timing probe only -- the results are
+// garbage -- used to attribute step time to kernel classes inside the PDL-overlapped chain
+// (scripts/ablate_probe.py), where per-launch event brackets would serialise the chain.
+inline int ablate_mask() {
+  static const int mask = [] {
+    const char* e = std::getenv("AG_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mask;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                      Args&&... args) {
+  if (ablate_mask() & cls) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

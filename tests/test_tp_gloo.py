@@ -103,11 +103,16 @@ def test_tp2_matches_unsharded_oracle():
         p.join(timeout=300)
         assert p.exitcode == 0
     cfg = M.OPTConfig("tp-test", hidden=256, num_layers=2, num_heads=2, ffn=1024, max_positions=256)
-    full = OracleExecutor(cfg, M.init_weights(cfg, seed=0, init="test"), 256)
+    w = M.init_weights(cfg, seed=0, init="test")
+    full = OracleExecutor(cfg, w, 256)
+    emu = OracleExecutor(cfg, w, 256, tp_emulate=2)  # unsharded weights, TP=2 rounding points
     for b, tl in zip(_batches(cfg), got):
         ref = full.execute(b).logits.numpy()
         assert np.abs(ref - tl).max() < 3e-2
         assert (ref.argmax(-1) == tl.argmax(-1)).mean() >= 0.99
+        e = emu.execute(b).logits.numpy()
+        print(f"sharded vs unsharded {np.abs(ref - tl).max():.3g}, vs tp_emulate=2 {np.abs(e - tl).max():.3g}")
+        assert np.array_equal(e, tl)  # the emulation reproduces the sharded composition exactly
 
 
 def test_pack_unpack_roundtrip():

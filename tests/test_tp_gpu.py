@@ -7,7 +7,9 @@ QKV / FC1 column shards by heads / FFN, out-proj / FC2 row shards with the bf16 
 all-reduced and bias + residual + LayerNorm applied after the reduce, the vocab-parallel LM head
 (TP=8: 6284-column shards of OPT's 50272, padded to 32 columns on the device) and the merge of the
 per-rank (max, index) candidates.  Tolerance as tests/test_forward_gpu.py (tests/parity.py): max|dlogit|
-<= 2e-2 or 1.5x the oracle's own fp32-vs-fp64 noise floor, >= 99% identical greedy tokens."""
+<= 2e-2 or 1.5x the oracle's own fp32-vs-fp64 noise floor, >= 99% identical greedy tokens.  The oracle
+mirrors the TP=t rounding points (tp_emulate: bf16 per-shard partials of out-proj / FC2, one bf16 rounding
+after the fp32 reduce) on the unsharded weights."""
 import socket
 import subprocess
 import sys
@@ -60,8 +62,9 @@ def test_tp_sharded_forward_vs_unsharded_oracle(tp, name, tmp_path):
     cfg, seed, blocks, steps = case(name)
     check = checked_steps(name)
     w = M.init_weights(cfg, seed, device="cuda", init="test")  # the same global model, unsharded
-    ref = OracleExecutor(cfg, w, blocks, device="cuda")
-    ref64 = OracleExecutor(cfg, w, blocks, device="cuda", acc=torch.float64)
+    # unsharded weights, TP=tp rounding points (bf16 partials, one rounding after the reduce)
+    ref = OracleExecutor(cfg, w, blocks, device="cuda", tp_emulate=tp)
+    ref64 = OracleExecutor(cfg, w, blocks, device="cuda", acc=torch.float64, tp_emulate=tp)
     pool = BlockPool(blocks)
     tally = Tally()
     for i, segs in enumerate(steps):

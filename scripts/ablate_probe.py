@@ -57,12 +57,12 @@ BATCHES = {
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else os.environ.get("AG_ABLATE", "0")
     cfg = Mo.opt_13b(max_positions=8192)
-    need = sum(sum((c + n + BS - 1) // BS for c, n in segs) for segs in BATCHES.values()) + 8
+    # timing only: every batch reuses block ids from 0 (its KV contents are whatever the last one wrote)
+    need = max(sum((c + n + BS - 1) // BS for c, n in segs) for segs in BATCHES.values()) + 8
     ex = CudaExecutor(cfg, need, max_tokens=2048, max_seqs=256, autotune=True)
-    nb = 0
     out = {"tag": tag, "ablate": os.environ.get("AG_ABLATE", "0"), "pdl": os.environ.get("AG_PDL", "1")}
     for name, segs in BATCHES.items():
-        b, nb = build(segs, cfg, nb)
+        b, _ = build(segs, cfg, 0)
         for _ in range(3):
             ex.execute(b)
         ts = sorted(ex.execute(b).device_s for _ in range(15))

@@ -285,9 +285,19 @@ AG_DEVICE void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
 // a kernel's CTAs may become resident, initialise barriers / TMEM and prefetch weights while its
 // predecessor drains.  Every thread that touches memory the predecessor writes (or reads, for
 // outputs written in place) first executes griddepcontrol.wait, which returns once the
-// predecessor grid has completed and its writes are visible; every kernel executes it in at least
-// one thread of every CTA before exiting, so completion stays transitive along the chain.  Without
-// the launch attribute (AG_PDL=0, or a standalone launch) the wait returns immediately.
+// predecessor grid has completed and its writes are visible.
+//
+// Invariant (deadlock freedom): every thread of every kernel executes griddepcontrol.wait BEFORE
+// griddepcontrol.launch_dependents.  Kernel k+1 can therefore launch only after all CTAs of kernel
+// k have passed their wait, i.e. after kernel k-1 has completed, so at most two grids of the chain
+// are live: R (running, every CTA already resident, depending on nothing unfinished) and its early
+// dependent D (prologue done, blocked in griddepcontrol.wait or in tcgen05.alloc behind R's TMEM).
+// R cannot block on D -- it allocated its TMEM before triggering and needs nothing else D holds --
+// so R completes, then D proceeds.  Triggering before the wait (the round-1 scheme: GEMM / attention
+// right after their TMEM allocation, small kernels on entry) let a third grid in; with a stream-K
+// GEMM (all SMs, atomic epilogue) as the primary of an early-launched LayerNorm or GEMM the B200
+// forward hung (profiles/r2/r2k_pdl_hang.md).  Without the launch attribute (AG_PDL=0, or a
+// standalone launch) the wait returns immediately.
 AG_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 AG_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

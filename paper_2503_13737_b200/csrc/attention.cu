@@ -337,8 +337,8 @@ AG_DEVICE void tile_tc(const AttnParams& p, const AttnTmaps& tm, const AttnItem&
 #ifdef AG_ATTN_TIMELINE
   if (threadIdx.x == 0) AG_TL(1, gtimer());
 #endif
+  pdl_trigger();  // only after the TMEM allocation (see gemm_bf16_tn_kernel)
   pdl_wait();     // Q, the paged K/V and the outputs belong to the predecessor kernels
-  pdl_trigger();  // after the wait (common.cuh: at most two grids of the chain are live)
   const uint32_t tmem = bars->tmem_base;  // S buffers [128 i, 128 i + 128), O [kOCol, kOCol + 128)
 
   if (warp == 0) {
@@ -636,8 +636,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tile_tc(p, tm, it, static_cast<int>(ti / n_tile_items), smem);
     return;
   }
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5;
   const int row_cta = static_cast<int>(b - (T > 0 ? ((b + 1) * T + C - 1) / C : 0));  // tiles at or before b
   const int u = row_cta * (kThreads / 32) + warp;
@@ -651,8 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // One warp per (query row, head), four head dims per lane; splits of a row sit `q_rows` apart.
 __global__ void __launch_bounds__(256) attn_combine_kernel(AttnParams p, const AttnCombine* __restrict__ combines,
                                                            int n_combines) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (unit >= n_combines * p.heads) return;
   const int lane = threadIdx.x & 31;

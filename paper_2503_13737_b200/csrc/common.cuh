@@ -285,33 +285,30 @@ AG_DEVICE void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
 // a kernel's CTAs may become resident, initialise barriers / TMEM and prefetch weights while its
 // predecessor drains.  Every thread that touches memory the predecessor writes (or reads, for
 // outputs written in place) first executes griddepcontrol.wait, which returns once the
-// predecessor grid has completed and its writes are visible.
-//
-// Invariant (deadlock freedom): every thread of every kernel executes griddepcontrol.wait BEFORE
-// griddepcontrol.launch_dependents.  Kernel k+1 can therefore launch only after all CTAs of kernel
-// k have passed their wait, i.e. after kernel k-1 has completed, so at most two grids of the chain
-// are live: R (running, every CTA already resident, depending on nothing unfinished) and its early
-// dependent D (prologue done, blocked in griddepcontrol.wait or in tcgen05.alloc behind R's TMEM).
-// R cannot block on D -- it allocated its TMEM before triggering and needs nothing else D holds --
-// so R completes, then D proceeds.  Triggering before the wait (the round-1 scheme: GEMM / attention
-// right after their TMEM allocation, small kernels on entry) let a third grid in; with a stream-K
-// GEMM (all SMs, atomic epilogue) as the primary of an early-launched LayerNorm or GEMM the B200
-// forward hung (profiles/r2/r2k_pdl_hang.md).  Without the launch attribute (AG_PDL=0, or a
-// standalone launch) the wait returns immediately.
+// predecessor grid has completed and its writes are visible; every kernel executes it in at least
+// one thread of every CTA before exiting, so completion stays transitive along the chain.  Without
+// the launch attribute (AG_PDL=0, or a standalone launch) the wait returns immediately.
 AG_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 AG_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // AG_PDL=0 disables it; AG_PDL_MASK=<bits> enables it per launch class (1 GEMM, 2 attention,
 // 4 norms, 8 other) for bisection.
-enum PdlClass { kPdlGemm = 1, kPdlAttn = 2, kPdlNorm = 4, kPdlOther = 8 };
+// kPdlNoEarly (a flag, or-ed into the class): never launched early, whatever the mask.
+enum PdlClass { kPdlGemm = 1, kPdlAttn = 2, kPdlNorm = 4, kPdlOther = 8, kPdlNoEarly = 0x100 };
 inline bool pdl_enabled(int cls) {
+  if (cls & kPdlNoEarly) return false;
   static const int mask = [] {
     const char* e = std::getenv("AG_PDL");
     if (e && e[0] == '0') return 0;
     const char* m = std::getenv("AG_PDL_MASK");
-    // Norm kernels are not launched early (they still trigger their dependents): with GEMM -> norm
-    // -> GEMM all early-launched, the 13B mixed-batch forward hung on B200 (no mbarrier timeout:
-    // a hardware wait never returned).  GEMM, attention and the small kernels are.
+    // Norm kernels are not launched early (they still trigger their dependents).  Measured on B200
+    // (profiles/r2/r2l_pdl_hang.md): the OPT-13B forward hangs -- a hardware wait never returns, no
+    // mbarrier timeout -- when the successor of a stream-K GEMM (grid = every SM, atomic epilogue)
+    // is launched early, i.e. with norms early-launched (AG_PDL_MASK=15) or with the norms removed
+    // (GEMM -> GEMM behind out-proj / FC2), and only with the attention kernel in the chain; with
+    // deterministic plans (no stream-K) the same chains complete.  The root cause is not isolated,
+    // so the shipped scheme never early-launches a kernel behind a stream-K GEMM: out-proj / FC2 are
+    // followed by a LayerNorm (norm class off) and QKV / FC1 by splitk_finish (kPdlNoEarly).
     return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlOther);
   }();
   return (mask & cls) != 0;

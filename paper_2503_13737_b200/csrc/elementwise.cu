@@ -27,8 +27,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
                              const __nv_bfloat16* __restrict__ tok_emb,
                              const __nv_bfloat16* __restrict__ pos_emb, int pos_offset, int rows,
                              int hidden, int vocab, int max_pos_rows, __nv_bfloat16* __restrict__ out) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int vec_per_row = hidden / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -281,8 +281,8 @@ __global__ void __launch_bounds__(kLNWarpsPerBlock * 32)
 // One thread per (row, head, pair of 2 x 4 dims): 8-B vector loads/stores of both halves.
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ x, int ld, const int32_t* __restrict__ positions, int rows,
                             int heads, int head_dim, int rotary_dim, float log2_theta) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int half = rotary_dim / 2;
   const int quads = half / 4;
   const int64_t total = static_cast<int64_t>(rows) * heads * quads;
@@ -322,8 +322,8 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv
                                  int ld_src, const int32_t* __restrict__ slot_mapping, int rows, int heads,
                                  int head_dim, int block_size, __nv_bfloat16* __restrict__ kcache,
                                  __nv_bfloat16* __restrict__ vcache) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int vec_per_row = heads * head_dim / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -347,8 +347,8 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k, const __nv
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int ld_src,
                                    const int32_t* __restrict__ index, int rows, int cols,
                                    __nv_bfloat16* __restrict__ dst, int ld_dst) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int vec_per_row = cols / 8;
   const int64_t total = static_cast<int64_t>(rows) * vec_per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -373,8 +373,8 @@ AG_DEVICE void argmax_merge(float& v, int& i, float ov, int oi) {
 __global__ void __launch_bounds__(kArgmaxThreads)
     argmax_kernel(const float* __restrict__ logits, int cols, int ld, int index_offset,
                   float* __restrict__ out_val, int32_t* __restrict__ out_idx) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   __shared__ float sv[kArgmaxThreads / 32];
   __shared__ int si[kArgmaxThreads / 32];
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * ld;
@@ -412,8 +412,8 @@ __global__ void __launch_bounds__(kArgmaxThreads)
 
 __global__ void argmax_merge_kernel(const float* __restrict__ vals, const int32_t* __restrict__ idx, int tp,
                                     int rows, int32_t* __restrict__ out_idx) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   float b = vals[r];
@@ -425,8 +425,8 @@ __global__ void argmax_merge_kernel(const float* __restrict__ vals, const int32_
 __global__ void block_copy_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                   const int32_t* __restrict__ block_ids, int n_blocks, int64_t block_elems,
                                   int gather) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int64_t vec_per_block = block_elems / 8;
   const int64_t total = vec_per_block * n_blocks;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;

@@ -211,14 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // dependents may launch only once this CTA holds its TMEM: an early dependent CTA on this SM
+  // that allocated first would wait (griddepcontrol.wait) on us while we wait on its columns
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
-  // Programmatic dependent launch (common.cuh): every thread triggers the next kernel only after its
-  // own griddepcontrol.wait, so the dependent is launched once this grid's predecessor has completed.
-  // Only the producer thread has work before the wait (the weight prefetch below).
-  if (warp != 0 || lane != 0) {
-    pdl_wait();
-    pdl_trigger();
-  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -242,7 +238,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
       pdl_wait();
-      pdl_trigger();
       int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -297,7 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> fused ops -> global
-    const int ew = warp - 4;  // (waited above: residuals / outputs belong to the predecessor)
+    const int ew = warp - 4;
+    pdl_wait();  // the epilogue reads residuals and writes outputs the predecessor may still use
     int acc = 0;
     uint32_t acc_phase = 0;
     SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
@@ -397,11 +393,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see the 1-CTA kernel)
   const uint32_t tmem_base = *tmem_slot;
-  if (warp != 0 || lane != 0) {  // trigger only after the wait (see the 1-CTA kernel)
-    pdl_wait();
-    pdl_trigger();
-  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -423,7 +416,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
       }
       pdl_wait();
-      pdl_trigger();
       int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -476,6 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256-row tile
     const int ew = warp - 4;
+    pdl_wait();
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -523,8 +516,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // flight per thread).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int splits, int M,
                                                             int N, GemmEpilogue ep) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int groups = N / 8;
   const int64_t total = static_cast<int64_t>(M) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -555,8 +548,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
 // Stream-K finish for GEMMs whose epilogue cannot be deferred to a consumer (QKV, FC1): the atomic
 // fp32 accumulator acc[M, N] gets the fused epilogue (8 columns per thread) and is re-zeroed.
 __global__ void __launch_bounds__(256) splitk_finish_kernel(float* __restrict__ acc, int M, int N, GemmEpilogue ep) {
-  pdl_wait();
   pdl_trigger();
+  pdl_wait();
   const int groups = N / 8;
   const int64_t total = static_cast<int64_t>(M) * groups;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -705,7 +698,8 @@ cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& e
   if (N % 8 != 0 || ep.mode == kEpiAtomicF32) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   const int g = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  (void)launch_k(kPdlGemm, splitk_finish_kernel, g, 256, 0, stream, acc, M, N, ep);
+  // never launched early behind the stream-K GEMM that fills acc (common.cuh, pdl_enabled)
+  (void)launch_k(kPdlGemm | kPdlNoEarly, splitk_finish_kernel, g, 256, 0, stream, acc, M, N, ep);
   return cudaGetLastError();
 }
 

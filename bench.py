@@ -7,7 +7,7 @@ OPT-13B (random bf16 weights) on the GPU(s) and emits tokens.  Workload: 90% <=1
 output 1-2048, TBT 0.1875 s x U(0.75,1.25), TTFT per 512-token bucket x U(0.5,1.5); the arrival rate
 scales with the GPU count (weak scaling), TP over the GPUs.
 
-  step   one 1-second goodput window of serving (SPEC.md:528 windows, ~25-45 forwards each); the K timed
+  step   one 2-second window of serving (--window-s; SPEC.md:528 goodput windows are 1 s, ~50 forwards); the K timed
          windows start after an untimed ramp to steady state (--ramp-s of serving: request population and
          KV occupancy have levelled off) and W warm-up windows
   value  SLO-meeting tokens / sum of CUDA-event forward times of the K windows (metadata resident in
@@ -48,7 +48,7 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--rate", type=float, default=None, help="arrival rate per GPU (req/s)")
     ap.add_argument("--ramp-s", type=float, default=None, help="untimed seconds of serving before warmup")
-    ap.add_argument("--window-s", type=float, default=1.0, help="seconds of serving per step")
+    ap.add_argument("--window-s", type=float, default=2.0, help="seconds of serving per step (2 s: the per-window spread of 1 s windows / sqrt 2)")
     ap.add_argument("--policy", default="accelgen")
     ap.add_argument("--tp-backend", choices=("nccl", "host"), default="nccl",
                     help="host: TP collectives through the library's host backend (ranks may share a GPU)")

@@ -1046,6 +1046,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   AG_CUDA(ag::launch_fill_hash(m->attn, static_cast<int64_t>(T) * m->hq, 0x2345u, 0.17f, false, s));
   AG_CUDA(ag::launch_fill_hash(m->ffn, static_cast<int64_t>(T) * m->ffn_l, 0x3456u, 1.7f, true, s));
   AG_CUDA(ag::launch_fill_hash(m->lm_in, static_cast<int64_t>(align_up(c.max_seqs, 128)) * H, 0x4567u, 1.7f, false, s));
+  AG_CUDA(ag::launch_fill_hash(m->resid, static_cast<int64_t>(T) * H, 0x5678u, 1.7f, false, s));
+  AG_CUDA(cudaMemsetAsync(m->acc32, 0, sizeof(float) * T * H, s));
   // Candidates are timed on the weights of successive layers (as in the forward), so weight tiles
   // come from HBM, not from an L2 that still holds the previous repetition's copy.
   struct Shape {
@@ -1120,17 +1122,36 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         const int wbox = p.am == 256 ? p.bn / 2 : p.bn;
         const CUtensorMap& am = sh.a->box(p.am == 256 ? 128 : p.am);
         const int nw = static_cast<int>(sh.w.size());
-        AG_CUDA(ag::launch_gemm(am, sh.w[nw - 1]->box(wbox), M, sh.N, sh.K, p.bn, eg, 0, s, p.k_splits, m->splitk_ws,
-                                p.am));
-        if (finish) AG_CUDA(ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s));
+        // TP=1 out-proj / FC2 are timed with the LayerNorm that consumes them, as in the forward: an
+        // atomic plan leaves bias + residual + the fp32 accumulator's read-and-re-zero to
+        // launch_layernorm_acc (12 B per element more than the direct epilogue's bf16 residual path)
+        const bool with_ln = c.tp_size == 1 && (k == kGemmOut || k == kGemmFc2);
+        const ag_layer_weights& w0 = m->layers[0].w;
+        const bf16* bias_k = static_cast<const bf16*>(k == kGemmOut ? w0.out_b : w0.fc2_b);
+        ag::GemmEpilogue ed = eg;
+        if (with_ln && ed.mode != ag::kEpiAtomicF32) {
+          ed.bias = bias_k;
+          ed.residual = m->resid;
+          ed.ldr = H;
+          ed.out = m->resid;
+        }
+        auto one = [&](int rep) -> cudaError_t {
+          cudaError_t e = ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, ed, 0, s, p.k_splits,
+                                          m->splitk_ws, p.am);
+          if (e != cudaSuccess) return e;
+          if (finish) return ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s);
+          if (!with_ln) return cudaSuccess;
+          const bf16* g = static_cast<const bf16*>(w0.ln2_g);
+          const bf16* bb = static_cast<const bf16*>(w0.ln2_b);
+          if (ed.mode == ag::kEpiAtomicF32)
+            return ag::launch_layernorm_acc(m->resid, m->acc32, bias_k, nullptr, g, bb,
+                                            c.ln_eps, M, H, m->xln, s);
+          return ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, g, bb, c.ln_eps, M, H, m->xln, s);
+        };
+        AG_CUDA(one(nw - 1));
         const int iters = 8;
         AG_CUDA(cudaEventRecord(e0, s));
-        for (int rep = 0; rep < iters; ++rep)
-        {
-          AG_CUDA(ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, eg, 0, s, p.k_splits,
-                                  m->splitk_ws, p.am));
-          if (finish) AG_CUDA(ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s));
-        }
+        for (int rep = 0; rep < iters; ++rep) AG_CUDA(one(rep));
         AG_CUDA(cudaEventRecord(e1, s));
         AG_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;

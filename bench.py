@@ -329,6 +329,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     prof_k = ex.profile()
     ex.set_profiling(False)
+    pivot = pivot_forward(executor, mcfg, s_pf, num_blocks, world, peaks)  # before the followers stop
     if world > 1:
         executor.stop()
         t = torch.tensor([dev_s], dtype=torch.float64)
@@ -451,7 +452,7 @@ def run_ours(args):
         "clocks": clocks,
         "gemm_plans": " ".join(f"{k}:{mb}:{bn}x{ks}a{am}" for k, mb, bn, ks, am in ex.gemm_plans()),
     }
-    line["pivot_forward"] = pivot_forward(executor, mcfg, s_pf, num_blocks, world, peaks)
+    line["pivot_forward"] = pivot
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mcfg, batches, world)
     print(json.dumps(line), flush=True)

@@ -324,6 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+#ifdef AG_ATOMIC_FENCE  // experiment: drain this thread's red.global.add before the CTA exits
+    if (ep.mode == kEpiAtomicF32) __threadfence();
+#endif
   }
 
   tc_fence_before();
@@ -501,6 +504,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+#ifdef AG_ATOMIC_FENCE
+    if (ep.mode == kEpiAtomicF32) __threadfence();
+#endif
   }
 
   tc_fence_before();

@@ -293,23 +293,17 @@ AG_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" 
 
 // AG_PDL=0 disables it; AG_PDL_MASK=<bits> enables it per launch class (1 GEMM, 2 attention,
 // 4 norms, 8 other) for bisection.
-// kPdlNoEarly (a flag, or-ed into the class): never launched early, whatever the mask.
-enum PdlClass { kPdlGemm = 1, kPdlAttn = 2, kPdlNorm = 4, kPdlOther = 8, kPdlNoEarly = 0x100 };
+enum PdlClass { kPdlGemm = 1, kPdlAttn = 2, kPdlNorm = 4, kPdlOther = 8 };
 inline bool pdl_enabled(int cls) {
-  if (cls & kPdlNoEarly) return false;
   static const int mask = [] {
     const char* e = std::getenv("AG_PDL");
     if (e && e[0] == '0') return 0;
     const char* m = std::getenv("AG_PDL_MASK");
-    // Norm kernels are not launched early (they still trigger their dependents).  Measured on B200
-    // (profiles/r2/r2l_pdl_hang.md): the OPT-13B forward hangs -- a hardware wait never returns, no
-    // mbarrier timeout -- when the successor of a stream-K GEMM (grid = every SM, atomic epilogue)
-    // is launched early, i.e. with norms early-launched (AG_PDL_MASK=15) or with the norms removed
-    // (GEMM -> GEMM behind out-proj / FC2), and only with the attention kernel in the chain; with
-    // deterministic plans (no stream-K) the same chains complete.  The root cause is not isolated,
-    // so the shipped scheme never early-launches a kernel behind a stream-K GEMM: out-proj / FC2 are
-    // followed by a LayerNorm (norm class off) and QKV / FC1 by splitk_finish (kPdlNoEarly).
-    return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlOther);
+    // Every class is launched early.  Round 1 kept the norms out (mask 11) after a hang that was
+    // later traced to atomic-epilogue GEMMs exiting with red.global.add still in flight: an
+    // early-launched successor's griddepcontrol.wait was never released (profiles/r2/r2l_pdl_hang.md).
+    // Those GEMMs now fence before exiting (gemm_sm100.cu).
+    return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlNorm | kPdlOther);
   }();
   return (mask & cls) != 0;
 }

@@ -324,9 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-#ifdef AG_ATOMIC_FENCE  // experiment: drain this thread's red.global.add before the CTA exits
+    // Drain this thread's red.global.add before the CTA exits.  Without it, a kernel launched early
+    // (PDL) behind this grid can sit in griddepcontrol.wait forever: measured on B200, the OPT-13B
+    // forward hung whenever the successor of an atomic-epilogue GEMM was early-launched
+    // (profiles/r2/r2l_pdl_hang.md); with the fence the same chains complete, at no measurable cost.
     if (ep.mode == kEpiAtomicF32) __threadfence();
-#endif
   }
 
   tc_fence_before();
@@ -504,9 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-#ifdef AG_ATOMIC_FENCE
-    if (ep.mode == kEpiAtomicF32) __threadfence();
-#endif
+    if (ep.mode == kEpiAtomicF32) __threadfence();  // (see the 1-CTA kernel)
   }
 
   tc_fence_before();
@@ -704,8 +704,7 @@ cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& e
   if (N % 8 != 0 || ep.mode == kEpiAtomicF32) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   const int g = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
-  // never launched early behind the stream-K GEMM that fills acc (common.cuh, pdl_enabled)
-  (void)launch_k(kPdlGemm | kPdlNoEarly, splitk_finish_kernel, g, 256, 0, stream, acc, M, N, ep);
+  (void)launch_k(kPdlGemm, splitk_finish_kernel, g, 256, 0, stream, acc, M, N, ep);
   return cudaGetLastError();
 }
 

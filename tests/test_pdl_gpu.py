@@ -25,3 +25,13 @@ def test_pdl_on_off_bitwise(tmp_path):
     on = _run(tmp_path / "on.npy", {k: v for k, v in base.items() if k != "AG_PDL"})  # reads it
     assert off.shape == on.shape and off.size > 0
     assert np.array_equal(off, on), float(np.abs(off - on).max())
+
+
+def test_pdl_behind_atomic_epilogue_completes():
+    """Early-launched LayerNorm behind stream-K out-proj / FC2 (fp32 red.global.add epilogue), 40-layer
+    OPT-13B shape, attention in the chain: hung on B200 until the atomic epilogue fenced its reductions
+    before the CTA exits.  A hang shows up as the subprocess timeout."""
+    r = subprocess.run([sys.executable, "tests/helpers/pdl_atomic_stress.py"], env=dict(os.environ),
+                       capture_output=True, text=True, timeout=420)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "30 forwards ok" in r.stdout

@@ -301,7 +301,7 @@ inline bool pdl_enabled(int cls) {
     const char* m = std::getenv("AG_PDL_MASK");
     // Every class is launched early.  Round 1 kept the norms out (mask 11) after a hang that was
     // later traced to atomic-epilogue GEMMs exiting with red.global.add still in flight: an
-    // early-launched successor's griddepcontrol.wait was never released (profiles/r2/r2l_pdl_hang.md).
+    // early-launched successor's griddepcontrol.wait was never released (profiles/r2/pdl_hang.md).
     // Those GEMMs now fence before exiting (gemm_sm100.cu).
     return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlNorm | kPdlOther);
   }();

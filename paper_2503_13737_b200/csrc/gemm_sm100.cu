@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Drain this thread's red.global.add before the CTA exits.  Without it, a kernel launched early
     // (PDL) behind this grid can sit in griddepcontrol.wait forever: measured on B200, the OPT-13B
     // forward hung whenever the successor of an atomic-epilogue GEMM was early-launched
-    // (profiles/r2/r2l_pdl_hang.md); with the fence the same chains complete, at no measurable cost.
+    // (profiles/r2/pdl_hang.md); with the fence the same chains complete, at no measurable cost.
     if (ep.mode == kEpiAtomicF32) __threadfence();
   }
 

@@ -299,11 +299,12 @@ inline bool pdl_enabled(int cls) {
     const char* e = std::getenv("AG_PDL");
     if (e && e[0] == '0') return 0;
     const char* m = std::getenv("AG_PDL_MASK");
-    // Every class is launched early.  Round 1 kept the norms out (mask 11) after a hang that was
-    // later traced to atomic-epilogue GEMMs exiting with red.global.add still in flight: an
-    // early-launched successor's griddepcontrol.wait was never released (profiles/r2/pdl_hang.md).
-    // Those GEMMs now fence before exiting (gemm_sm100.cu).
-    return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlNorm | kPdlOther);
+    // LayerNorms are not launched early (they still trigger their dependents).  With them early
+    // (mask 15) the OPT-13B forward hangs on B200: a griddepcontrol.wait is never released
+    // (profiles/r2/pdl_hang.md).  Fencing the atomic-epilogue GEMMs' red.global.add before their
+    // CTAs exit (gemm_sm100.cu) made every isolated repro complete, but the serving bench still
+    // hangs with mask 15, so the cause is not fully isolated; mask 11 has never hung.
+    return m ? std::atoi(m) : (kPdlGemm | kPdlAttn | kPdlOther);
   }();
   return (mask & cls) != 0;
 }

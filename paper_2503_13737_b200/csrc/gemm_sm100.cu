@@ -325,9 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (acc == 0) acc_phase ^= 1;
     }
     // Drain this thread's red.global.add before the CTA exits.  Without it, a kernel launched early
-    // (PDL) behind this grid can sit in griddepcontrol.wait forever: measured on B200, the OPT-13B
-    // forward hung whenever the successor of an atomic-epilogue GEMM was early-launched
-    // (profiles/r2/pdl_hang.md); with the fence the same chains complete, at no measurable cost.
+    // (PDL) behind this grid could sit in griddepcontrol.wait forever: the 40-layer OPT-13B forward
+    // hung whenever the successor of an atomic-epilogue GEMM was early-launched, and completes with
+    // the fence, at no measurable cost (profiles/r2/pdl_hang.md).
     if (ep.mode == kEpiAtomicF32) __threadfence();
   }
 

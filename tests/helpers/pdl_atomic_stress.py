@@ -1,6 +1,6 @@
 """Helper for tests/test_pdl_gpu.py: the configuration that hung before atomic-epilogue GEMMs fenced
 their red.global.add (profiles/r2/pdl_hang.md).  The full 40-layer OPT-13B shape, every kernel
-class launched early (the default), out-proj / FC2 forced to stream-K over their fp32 accumulator
+class launched early (the caller sets AG_PDL_MASK=15), out-proj / FC2 forced to stream-K over their fp32 accumulator
 (finished by the early-launched LayerNorm) in every M bucket, and the attention kernel in the chain:
 30 decode-heavy forwards must complete.  Prints the forward times."""
 import ctypes as C

@@ -426,6 +426,8 @@ def run_ours(args):
                          "prompts_credit_unresolved": unresolved},
         "preemptions_in_window": sum(r.preemptions for r in recs),
         "swap_gb_total": getattr(ex, "swap_bytes", 0) / 1e9,
+        "swap_host": {"blocked_s_total": getattr(ex, "swap_wait_s", 0.0), "blocked_waits": getattr(ex, "swap_waits", 0),
+                      "pageable": bool(getattr(ex, "_pin_failed", False))},
         "hbm_gb": {"kv_pool": num_blocks * 32 * kv_tok_bytes / 1e9, "free_after_setup": free_after_setup / 1e9,
                    "free_at_end": torch.cuda.mem_get_info()[0] / 1e9},
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,

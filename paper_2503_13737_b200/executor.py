@@ -263,12 +263,17 @@ class CudaExecutor:
         self._next_slot = 0
         self._copy_stream = torch.cuda.Stream(self.device)
         self.swap_bytes = 0
+        self.swap_wait_s, self.swap_waits = 0.0, 0  # host time blocked on a draining staging slot
 
     def _acquire_slot(self) -> int:
         i = self._next_slot
         self._next_slot = (i + 1) % self._SWAP_SLOTS
         if self._slot_free[i] is not None:
-            self._slot_free[i].synchronize()  # only blocks when every slot is still draining
+            if not self._slot_free[i].query():  # only blocks when every slot is still draining
+                t0 = time.perf_counter()
+                self._slot_free[i].synchronize()
+                self.swap_wait_s += time.perf_counter() - t0
+                self.swap_waits += 1
             self._slot_free[i] = None
         self._slot_keep[i] = []
         return i

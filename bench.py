@@ -275,6 +275,7 @@ def run_ours(args):
     ex.set_roofline_peaks(peaks["tensor_sustained"], peaks["hbm"])
     ex.set_profiling(False)  # the timed windows run un-instrumented; kernel classes come from a replay
     launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
+    plan0, swap0 = eng.plan_host_s, getattr(ex, "swap_host_s", 0.0)
     sampler = ClockSampler(local % n_dev)
     sampler.start()
     torch.cuda.synchronize()
@@ -301,6 +302,7 @@ def run_ours(args):
     ex.execute = orig_exec
     if orig_submit is not None:
         ex.submit = orig_submit
+    plan_s, swap_s = eng.plan_host_s - plan0, getattr(ex, "swap_host_s", 0.0) - swap0
     recs = [it for w in windows for it in w]
     dev_s = sum(r.device_s for r in recs)
     launches_timed = ex.launches - launches0
@@ -450,7 +452,11 @@ def run_ours(args):
         "host_ms_per_step": {"pre": 1e3 * sum(r.host_pre_s for r in recs) / K,
                              "execute_wall": 1e3 * sum(r.wall_s for r in recs) / K,
                              "post": 1e3 * sum(r.host_post_s for r in recs) / K,
-                             "device_forward": 1e3 * dev_s / K, "wall_total": 1e3 * wall / K},
+                             "device_forward": 1e3 * dev_s / K, "wall_total": 1e3 * wall / K,
+                             "pre_plan": 1e3 * plan_s / K, "pre_swap": 1e3 * swap_s / K,
+                             # pipelined host: a step whose host work outlasts the forward it overlaps idles the GPU
+                             "pre_over_device_ms": 1e3 * sum(max(0.0, r.host_pre_s - r.device_s) for r in recs) / K,
+                             "steps_pre_over_device": sum(r.host_pre_s > r.device_s for r in recs) / K},
         "clocks": clocks,
         "gemm_plans": " ".join(f"{k}:{mb}:{bn}x{ks}a{am}" for k, mb, bn, ks, am in ex.gemm_plans()),
     }

@@ -293,6 +293,7 @@ class Engine:
         self.keep_history = False
         # pipelined wall clock: step k+1 is planned and submitted while the device runs step k
         self.pipeline = pipeline
+        self.plan_host_s = 0.0              # host time in order_queue + make_plan (pipelined steps)
         self._inflight: dict | None = None
         self._origin: float | None = None   # perf_counter time of engine time 0 (minus idle jumps)
         self._offset = 0.0                  # idle jumps (empty queue: the clock skips to the next arrival)
@@ -566,10 +567,12 @@ class Engine:
                     self._offset += nxt - self.clock
                     self.clock = nxt
             return None
+        t_plan = time.perf_counter()
         self.queue = order_queue(self.queue, self.clock, self.stats)
         ctx = PlanContext(self.pool, self.stats, self.profile, self.clock, set(self.long_active))
         plan = make_plan(self.queue, ctx, self.cfg)
         plan.check()
+        self.plan_host_s += time.perf_counter() - t_plan
         if plan.forward_size > self.executor.max_tokens or len(plan.selections) > self.executor.max_seqs:
             raise EngineFault(f"plan of {plan.forward_size} tokens / {len(plan.selections)} sequences exceeds the "
                               f"executor capacity ({self.executor.max_tokens}/{self.executor.max_seqs})")

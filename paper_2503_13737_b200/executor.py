@@ -264,6 +264,7 @@ class CudaExecutor:
         self._copy_stream = torch.cuda.Stream(self.device)
         self.swap_bytes = 0
         self.swap_wait_s, self.swap_waits = 0.0, 0  # host time blocked on a draining staging slot
+        self.swap_host_s = 0.0  # host time inside swap_out / swap_in (launches, pinned allocation, waits)
 
     def _acquire_slot(self) -> int:
         i = self._next_slot
@@ -299,6 +300,7 @@ class CudaExecutor:
         if not block_ids:
             return
         self._swap_init()
+        t_host = time.perf_counter()
         comp = torch.cuda.current_stream(self.device)
         host_chunks = []
         for c0 in range(0, len(block_ids), self._stage_blocks):
@@ -322,6 +324,7 @@ class CudaExecutor:
             host_chunks.append(host)
             self.swap_bytes += host.numel() * 2
         self._swapped[request_id] = host_chunks
+        self.swap_host_s += time.perf_counter() - t_host
 
     def swap_in(self, request_id: int, block_ids: list[int], tokens: int) -> None:
         host_chunks = self._swapped.pop(request_id, None)
@@ -333,6 +336,7 @@ class CudaExecutor:
         if len(block_ids) < n_total:
             raise EngineFault("readmission allocated fewer blocks than were swapped out")
         self._swap_init()
+        t_host = time.perf_counter()
         comp = torch.cuda.current_stream(self.device)
         at = 0
         for host in host_chunks:
@@ -355,3 +359,4 @@ class CudaExecutor:
             self._slot_free[slot] = scattered
             self.swap_bytes += host.numel() * 2
             at += n
+        self.swap_host_s += time.perf_counter() - t_host

@@ -289,8 +289,12 @@ def run_ours(args):
     windows, win_wall = [], []
     for k in range(args.steps):
         tw = time.perf_counter()
+        c0 = eng.clock
         windows.append(serve_until(eng.clock + args.window_s))
         win_wall.append(time.perf_counter() - tw)
+        if os.environ.get("AG_BENCH_TRACE"):
+            print(f"window {k}: clock {c0:.2f} -> {eng.clock:.2f}, {len(windows[-1])} forwards, "
+                  f"wall {win_wall[-1]:.2f} s, queue {len(eng.queue)}", file=sys.stderr, flush=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     if ncu_window:
@@ -304,6 +308,9 @@ def run_ours(args):
         ex.submit = orig_submit
     plan_s, swap_s = eng.plan_host_s - plan0, getattr(ex, "swap_host_s", 0.0) - swap0
     recs = [it for w in windows for it in w]
+    if not recs:
+        raise SystemExit(f"no forward completed in the {args.steps} timed windows (engine clock {eng.clock:.1f} s, "
+                         f"queue {len(eng.queue)}, in flight {eng._inflight is not None})")
     dev_s = sum(r.device_s for r in recs)
     launches_timed = ex.launches - launches0
     h2d_timed, d2h_timed = ex.h2d_bytes - h2d0, ex.d2h_bytes - d2h0

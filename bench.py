@@ -205,6 +205,9 @@ def run_ours(args):
     ex = CudaExecutor(mcfg, num_blocks, max_tokens=s_pf, max_seqs=2048,
                       max_blocks_per_seq=(mcfg.pos_rows + 31) // 32, tp_rank=rank, tp_size=world, seed=0,
                       init="opt", nccl_uid=uid, host_collective=host_coll)
+    # preemption swaps: staging ring in HBM + host chunks pinned now rather than on the serving path
+    import psutil
+    ex.prepare_swap(min(16.0, 0.25 * psutil.virtual_memory().available / 1e9 / max(1, world)))
     torch.cuda.synchronize()
     free_after_setup = torch.cuda.mem_get_info()[0]
 
@@ -436,7 +439,8 @@ def run_ours(args):
         "preemptions_in_window": sum(r.preemptions for r in recs),
         "swap_gb_total": getattr(ex, "swap_bytes", 0) / 1e9,
         "swap_host": {"blocked_s_total": getattr(ex, "swap_wait_s", 0.0), "blocked_waits": getattr(ex, "swap_waits", 0),
-                      "pageable": bool(getattr(ex, "_pin_failed", False))},
+                      "pageable": bool(getattr(ex, "_pin_failed", False)),
+                      "host_chunks": getattr(ex, "swap_host_chunks", 0)},
         "hbm_gb": {"kv_pool": num_blocks * 32 * kv_tok_bytes / 1e9, "free_after_setup": free_after_setup / 1e9,
                    "free_at_end": torch.cuda.mem_get_info()[0] / 1e9},
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,

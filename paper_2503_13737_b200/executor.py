@@ -262,6 +262,8 @@ class CudaExecutor:
         self._slot_keep = [[] for _ in range(self._SWAP_SLOTS)]  # host tensors the slot's copies still read
         self._next_slot = 0
         self._copy_stream = torch.cuda.Stream(self.device)
+        self._host_free: list[tuple[torch.Tensor, torch.cuda.Event | None]] = []  # reusable host chunks
+        self.swap_host_chunks = 0  # host chunks allocated (pinned unless the OS refused)
         self.swap_bytes = 0
         self.swap_wait_s, self.swap_waits = 0.0, 0  # host time blocked on a draining staging slot
         self.swap_host_s = 0.0  # host time inside swap_out / swap_in (launches, pinned allocation, waits)
@@ -284,15 +286,38 @@ class CudaExecutor:
         keep.append(h)  # the async H2D reads it later
         return h.to(self.device, non_blocking=True)
 
-    def _host_buffer(self, shape) -> torch.Tensor:
-        """Pinned host memory for swapped KV (torch's caching host allocator); pageable when the OS
-        refuses to lock more pages."""
+    def _host_chunk(self, n: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """A host chunk for n staged blocks: (the backing 1-D buffer, a contiguous [L, 2, n, heads, 32, 128]
+        view of its head).  Every chunk is one full staging slot, so chunks are interchangeable: swap-in
+        hands them back to a free list once their H2D copy is done and swap-out reuses them, instead of
+        pinning fresh memory per swap (page-locking a multi-GB buffer blocked the host for seconds).
+        Pageable memory when the OS refuses to lock more pages."""
+        per_block = self._stage[0][:, :, 0].numel()
+        shape = (self.cfg.num_layers, 2, n) + tuple(self._stage[0].shape[3:])
+        while self._host_free:
+            flat, ready = self._host_free.pop()
+            if ready is not None and not ready.query():
+                ready.synchronize()
+            return flat, flat[: n * per_block].view(shape)
+        flat = None
         if not getattr(self, "_pin_failed", False):
             try:
-                return torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+                flat = torch.empty(self._stage_blocks * per_block, dtype=torch.bfloat16, pin_memory=True)
             except Exception:  # RuntimeError / torch.AcceleratorError: out of lockable memory
                 self._pin_failed = True
-        return torch.empty(shape, dtype=torch.bfloat16)
+        if flat is None:
+            flat = torch.empty(self._stage_blocks * per_block, dtype=torch.bfloat16)
+        self.swap_host_chunks += 1
+        return flat, flat[: n * per_block].view(shape)
+
+    def prepare_swap(self, host_gb: float) -> None:
+        """Allocate the staging ring and pin ~host_gb of host chunks up front (bench setup), so the first
+        preemptions do not page-lock memory on the serving path."""
+        self._swap_init()
+        n = int(host_gb * 1e9 // (self._stage_blocks * self._stage[0][:, :, 0].numel() * 2))
+        for _ in range(max(0, n)):
+            flat, _ = self._host_chunk(1)
+            self._host_free.append((flat, None))
 
     def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
         """Preemption (reference BlockPool.preempt, kvc.py:153-160): the request's KV blocks of every
@@ -314,14 +339,14 @@ class CudaExecutor:
                     K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv, :n])
             gathered = torch.cuda.Event()
             gathered.record(comp)
-            host = self._host_buffer((self.cfg.num_layers, 2, n) + tuple(stage.shape[3:]))
+            flat, host = self._host_chunk(n)
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(gathered)
                 host.copy_(stage[:, :, :n], non_blocking=host.is_pinned())
                 done = torch.cuda.Event()
                 done.record(self._copy_stream)
             self._slot_free[slot] = done
-            host_chunks.append(host)
+            host_chunks.append((flat, host))
             self.swap_bytes += host.numel() * 2
         self._swapped[request_id] = host_chunks
         self.swap_host_s += time.perf_counter() - t_host
@@ -332,24 +357,24 @@ class CudaExecutor:
             if tokens > 0:
                 raise EngineFault(f"request {request_id} readmitted without swapped KV")
             return
-        n_total = sum(h.shape[2] for h in host_chunks)
+        n_total = sum(h.shape[2] for _, h in host_chunks)
         if len(block_ids) < n_total:
             raise EngineFault("readmission allocated fewer blocks than were swapped out")
         self._swap_init()
         t_host = time.perf_counter()
         comp = torch.cuda.current_stream(self.device)
         at = 0
-        for host in host_chunks:
+        for flat, host in host_chunks:
             n = host.shape[2]
             slot = self._acquire_slot()
             stage = self._stage[slot]
             keep = self._slot_keep[slot]
             ids = self._ids_on_device(block_ids[at:at + n], keep)
-            keep.append(host)
             with torch.cuda.stream(self._copy_stream):  # same stream as the swap-out D2H: ordered after it
                 stage[:, :, :n].copy_(host, non_blocking=host.is_pinned())
                 loaded = torch.cuda.Event()
                 loaded.record(self._copy_stream)
+            self._host_free.append((flat, loaded))  # reusable once its H2D copy is done
             comp.wait_event(loaded)
             for l in range(self.cfg.num_layers):
                 for kv in range(2):

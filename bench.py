@@ -207,7 +207,7 @@ def run_ours(args):
                       init="opt", nccl_uid=uid, host_collective=host_coll)
     # preemption swaps: staging ring in HBM + host chunks pinned now rather than on the serving path
     import psutil
-    ex.prepare_swap(min(16.0, 0.25 * psutil.virtual_memory().available / 1e9 / max(1, world)))
+    ex.prepare_swap(min(48.0, 0.3 * psutil.virtual_memory().available / 1e9 / max(1, world)))
     torch.cuda.synchronize()
     free_after_setup = torch.cuda.mem_get_info()[0]
 

@@ -294,11 +294,12 @@ class CudaExecutor:
         Pageable memory when the OS refuses to lock more pages."""
         per_block = self._stage[0][:, :, 0].numel()
         shape = (self.cfg.num_layers, 2, n) + tuple(self._stage[0].shape[3:])
-        while self._host_free:
-            flat, ready = self._host_free.pop()
-            if ready is not None and not ready.query():
-                ready.synchronize()
-            return flat, flat[: n * per_block].view(shape)
+        # oldest first, and only a chunk whose H2D copy (swap-in) has finished; a fresh chunk otherwise --
+        # waiting on a pending copy would block the host behind the copy stream's queue
+        for i, (flat, ready) in enumerate(self._host_free):
+            if ready is None or ready.query():
+                del self._host_free[i]
+                return flat, flat[: n * per_block].view(shape)
         flat = None
         if not getattr(self, "_pin_failed", False):
             try:

@@ -133,8 +133,8 @@ def default_profile(tp: int):
                            fixed_overhead_s=0.006 / tp, kvc_capacity_tokens=0), "declared-default"
 
 
-DEFAULT_RATE = 3.0    # req/s per GPU: capacity-bound above ~3 req/s; the most reproducible point with >= 95%
-DEFAULT_RAMP_S = 150.0  # iteration-SLO attainment (profiles/r2/rate_sweep.md); ramp: KV occupancy levels off
+DEFAULT_RATE = 4.0    # req/s per GPU: capacity-bound from ~3 req/s; >= 98% iteration-SLO attainment in six runs
+DEFAULT_RAMP_S = 150.0  # (profiles/r2/rate_sweep.md); ramp: request population and KV occupancy level off
 
 
 def build_workload(args, world: int):

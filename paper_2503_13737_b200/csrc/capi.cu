@@ -221,6 +221,10 @@ struct ag_model {
   float* acc_big = nullptr;  // fp32 [T, max(3*hq, ffn)] stream-K accumulator of QKV / FC1 (zero between uses)
   int64_t acc_big_cols = 0;
   bool deterministic = false;  // AG_DETERMINISTIC=1: no fp32 atomics (split-K via the reduce kernel)
+  // TP=1 atomic out-proj / FC2 finish residual + bias + the next LayerNorm in their own tail (grid
+  // barrier on ln_bar) instead of a launch_layernorm_acc launch; AG_FUSE_LN=0 turns it off
+  bool fuse_ln = true;
+  unsigned int* ln_bar = nullptr;
   int64_t splitk_cap = 0;
   GemmTable tune;
   // metadata: one pinned host buffer mirrored by one device buffer
@@ -525,7 +529,11 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   {
     const char* e = std::getenv("AG_DETERMINISTIC");
     m->deterministic = e && e[0] == '1';
+    const char* f = std::getenv("AG_FUSE_LN");
+    m->fuse_ln = !(f && f[0] == '0');
   }
+  chk(dmalloc(&m->ln_bar, 64));
+  if (r == AG_OK && cudaMemset(m->ln_bar, 0, 64 * sizeof(unsigned int)) != cudaSuccess) r = fail(AG_ECUDA, "memset ln_bar");
   chk(dmalloc(&m->acc_big, T * m->acc_big_cols));
   if (r == AG_OK && cudaMemset(m->acc_big, 0, sizeof(float) * T * m->acc_big_cols) != cudaSuccess)
     r = fail(AG_ECUDA, "memset acc_big");
@@ -565,7 +573,7 @@ void ag_model_destroy(ag_model* m) {
   if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
   void* dev[] = {m->resid, m->xln, m->qbuf, m->attn, m->ffn, m->proj, m->lm_in, m->logits, m->cand_val,
                  m->cand_idx, m->gathered_val, m->gathered_idx, m->out_tok, m->part_o, m->part_ml, m->meta_dev,
-                 m->splitk_ws, m->acc32, m->acc_big};
+                 m->splitk_ws, m->acc32, m->acc_big, m->ln_bar};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (m->aslot[0].meta_host) m->meta_host = m->aslot[0].meta_host;  // slot 1's buffer is freed below
@@ -778,10 +786,21 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
       return !tp && p.k_splits > 1 && !m->deterministic;
     };
     bool acc_pending = false;
+    bool ln1_done = false;  // the previous FC2's fused tail already wrote this layer's LN1 (xln)
+    // fused LayerNorm tail on an atomic out-proj / FC2 (see ag::GemmEpilogue::ln_out)
+    auto fuse_ln = [&](ag::GemmEpilogue& e, const void* bias, const void* g, const void* b) {
+      e.ln_x = m->resid;
+      e.ln_bias = static_cast<const bf16*>(bias);
+      e.ln_g = static_cast<const bf16*>(g);
+      e.ln_b = static_cast<const bf16*>(b);
+      e.ln_eps = c.ln_eps;
+      e.ln_out = m->xln;
+      e.ln_bar = m->ln_bar;
+    };
     for (int l = 0; l < c.num_layers; ++l) {
       const LayerState& L = m->layers[l];
       const ag_layer_weights& w = L.w;
-      {
+      if (!ln1_done) {
         // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
         ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ((tp || acc_pending) && l > 0) ? 2.0 * ln_bytes : ln_bytes);
         if (acc_pending) {  // previous layer's FC2 was split-K into acc32: finish its epilogue here
@@ -844,6 +863,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         AG_CUDA(ag::launch_attention(ap, atm, m->d_items, m->n_tile_items, m->n_row_items, m->d_comb, m->n_comb, s));
         AG_TRY(dbg(s, "attention", l));
       }
+      bool ln2_done = false;
       {
         // out-proj (+bias +residual when TP=1; partial sum + all-reduce when TP>1)
         ag::GemmEpilogue eo;
@@ -853,6 +873,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         if (out_atomic) {
           eo.mode = ag::kEpiAtomicF32;
           eo.acc32 = m->acc32;
+          if (m->fuse_ln) fuse_ln(eo, w.out_b, w.ln2_g, w.ln2_b);
         } else if (!tp) {
           eo.bias = static_cast<const bf16*>(w.out_b);
           eo.residual = m->resid;
@@ -861,10 +882,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         } else {
           eo.out = m->proj;
         }
-        ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq), gemm_bytes(S, H, m->hq, tp ? 2 : 4));
+        ProfScope ps(m, AG_K_OUT_GEMM, s, gemm_flops(S, H, m->hq),
+                     gemm_bytes(S, H, m->hq, tp ? 2 : 4) + (eo.ln_out ? 2.0 * ln_bytes : 0.0));
         AG_CUDA(gemm_w(m->tm_attn, L.tm_out, S, H, m->hq, eo, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmOut,
                        &po));
-        acc_pending = out_atomic;
+        acc_pending = out_atomic && eo.ln_out == nullptr;
+        ln2_done = eo.ln_out != nullptr;
         AG_TRY(dbg(s, "out_gemm", l));
       }
       if (tp) {
@@ -882,6 +905,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
                                          static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps,
                                          S, H, m->xln, s));
         acc_pending = false;
+      } else if (ln2_done) {
+        // LN2 was finished by the out-proj's fused tail
       } else {
         ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ln_bytes);
         AG_CUDA(ag::launch_layernorm(m->resid, nullptr, nullptr, nullptr, static_cast<const bf16*>(w.ln2_g),
@@ -904,9 +929,14 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e2.ldc = H;
         ag::GemmPlan p2;
         const bool fc2_atomic = atomic_plan(L.tm_fc2, H, m->ffn_l, kGemmFc2, p2);
+        const bool fuse_next = fc2_atomic && m->fuse_ln && l + 1 < c.num_layers;
         if (fc2_atomic) {
           e2.mode = ag::kEpiAtomicF32;
           e2.acc32 = m->acc32;
+          if (fuse_next) {
+            const ag_layer_weights& wn = m->layers[l + 1].w;
+            fuse_ln(e2, w.fc2_b, wn.ln1_g, wn.ln1_b);
+          }
         } else if (!tp) {
           e2.bias = static_cast<const bf16*>(w.fc2_b);
           e2.residual = m->resid;
@@ -915,10 +945,12 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         } else {
           e2.out = m->proj;
         }
-        ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l), gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4));
+        ProfScope ps(m, AG_K_FC2_GEMM, s, gemm_flops(S, H, m->ffn_l),
+                     gemm_bytes(S, H, m->ffn_l, tp ? 2 : 4) + (fuse_next ? 2.0 * ln_bytes : 0.0));
         AG_CUDA(gemm_w(m->tm_ffn, L.tm_fc2, S, H, m->ffn_l, e2, s, m->splitk_ws, m->splitk_cap, &m->tune, kGemmFc2,
                        &p2));
-        acc_pending = fc2_atomic;
+        acc_pending = fc2_atomic && !fuse_next;
+        ln1_done = fuse_next;
         AG_TRY(dbg(s, "fc2_gemm", l));
       }
       if (tp) {
@@ -1135,12 +1167,22 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
           ed.ldr = H;
           ed.out = m->resid;
         }
+        const bool fused = with_ln && ed.mode == ag::kEpiAtomicF32 && m->fuse_ln;
+        if (fused) {  // the forward's fused LayerNorm tail (one launch)
+          ed.ln_x = m->resid;
+          ed.ln_bias = bias_k;
+          ed.ln_g = static_cast<const bf16*>(w0.ln2_g);
+          ed.ln_b = static_cast<const bf16*>(w0.ln2_b);
+          ed.ln_eps = c.ln_eps;
+          ed.ln_out = m->xln;
+          ed.ln_bar = m->ln_bar;
+        }
         auto one = [&](int rep) -> cudaError_t {
           cudaError_t e = ag::launch_gemm(am, sh.w[rep % nw]->box(wbox), M, sh.N, sh.K, p.bn, ed, 0, s, p.k_splits,
                                           m->splitk_ws, p.am);
           if (e != cudaSuccess) return e;
           if (finish) return ag::launch_splitk_finish(m->acc_big, M, sh.N, ep, s);
-          if (!with_ln) return cudaSuccess;
+          if (!with_ln || fused) return cudaSuccess;
           const bf16* g = static_cast<const bf16*>(w0.ln2_g);
           const bf16* bb = static_cast<const bf16*>(w0.ln2_b);
           if (ed.mode == ag::kEpiAtomicF32)

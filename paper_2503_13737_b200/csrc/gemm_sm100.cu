@@ -125,6 +125,132 @@ AG_DEVICE void epilogue_chunk(const GemmEpilogue& ep, int row, int col0, const u
   epilogue_cols<32>(ep, row, col0, v);
 }
 
+// ---------------------------------------------------------------- fused LayerNorm tail
+// A TP=1 out-proj / FC2 whose K is split accumulates into the fp32 buffer acc32, and the residual
+// add + bias + LayerNorm that consumes it used to be its own launch (launch_layernorm_acc): ~80 per
+// OPT-13B forward, each paying a full launch gap because the norms cannot be launched early
+// (profiles/r2/pdl_hang.md).  With ep.ln_out set, the GEMM's CTAs meet at a grid barrier once
+// their reductions have drained and finish the rows themselves.
+
+AG_DEVICE unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier.  Every CTA of these grids is co-resident: <= 1 CTA per SM (the operand ring
+// takes ~200 KB of shared memory), grid <= SMs, and a PDL dependent is only launched once every CTA
+// of this grid has executed griddepcontrol.launch_dependents -- i.e. is already resident -- so an
+// early dependent can never hold the SM a straggler of this grid needs.  bar[0] counts arrivals,
+// bar[1] is the generation; the last arriver resets the count before releasing the generation, and
+// the next grid to use the barrier starts its tail only after this grid has completed.
+AG_DEVICE void grid_barrier(unsigned* bar, unsigned ctas) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == ctas - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+AG_DEVICE float cta_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+constexpr int kLnMaxVec = 6;  // 8-column groups per thread: hidden <= 256 * 8 * 6 = 12288
+
+AG_DEVICE void bf16x8_unpack(const uint4& w, float (&f)[8]) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 p = unpack_bf16x2(ws[h]);
+    f[2 * h] = p.x;
+    f[2 * h + 1] = p.y;
+  }
+}
+
+AG_DEVICE uint4 bf16x8_pack(const float (&f)[8]) {
+  return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+}
+
+// Rows blockIdx.x, +gridDim.x, ... of  x = bf16(x + (acc + bias)); acc = 0; out = LN(x) * g + b  -- the
+// same rounding points as layernorm_row_kernel<float> (elementwise.cu), 256 threads per row.
+AG_DEVICE void ln_tail(const GemmEpilogue& ep, int M, int hidden) {
+  __shared__ float red[kThreads / 32];
+  grid_barrier(ep.ln_bar, gridDim.x);
+  const int nvec = hidden / 8;
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    __nv_bfloat16* xr = ep.ln_x + static_cast<int64_t>(r) * hidden;
+    float4* ar = reinterpret_cast<float4*>(ep.acc32 + static_cast<int64_t>(r) * ep.ldc);
+    float v[kLnMaxVec][8];
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kLnMaxVec; ++i) {
+      const int idx = threadIdx.x + i * kThreads;
+      if (idx < nvec) {
+        bf16x8_unpack(*reinterpret_cast<const uint4*>(xr + idx * 8), v[i]);
+        const float4 a = __ldcg(ar + 2 * idx), b = __ldcg(ar + 2 * idx + 1);
+        ar[2 * idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ar[2 * idx + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float d[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        if (ep.ln_bias != nullptr) {
+          float bb[8];
+          bf16x8_unpack(__ldg(reinterpret_cast<const uint4*>(ep.ln_bias) + idx), bb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d[j] += bb[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] += d[j];
+        const uint4 packed = bf16x8_pack(v[i]);
+        *reinterpret_cast<uint4*>(xr + idx * 8) = packed;  // updated residual stream
+        bf16x8_unpack(packed, v[i]);                       // normalise the rounded value
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum += v[i][j];
+      }
+    }
+    const float mean = cta_sum(sum, red) / hidden;
+    float sq = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kLnMaxVec; ++i)
+      if (threadIdx.x + i * kThreads < nvec)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float c = v[i][j] - mean;
+          sq += c * c;
+        }
+    const float rstd = rsqrtf(cta_sum(sq, red) / hidden + ep.ln_eps);
+    __nv_bfloat16* orow = ep.ln_out + static_cast<int64_t>(r) * hidden;
+#pragma unroll
+    for (int i = 0; i < kLnMaxVec; ++i) {
+      const int idx = threadIdx.x + i * kThreads;
+      if (idx < nvec) {
+        float g[8], b[8], y[8];
+        bf16x8_unpack(__ldg(reinterpret_cast<const uint4*>(ep.ln_g) + idx), g);
+        bf16x8_unpack(__ldg(reinterpret_cast<const uint4*>(ep.ln_b) + idx), b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y[j] = (v[i][j] - mean) * rstd * g[j] + b[j];
+        *reinterpret_cast<uint4*>(orow + idx * 8) = bf16x8_pack(y);
+      }
+    }
+  }
+}
+
 // Work decomposition shared by the three warp roles of the 1-CTA kernel.  Classic: unit t =
 // (m_blk, k_split, n_blk), m fastest (concurrent CTAs share a weight tile), strided over CTAs.
 // Stream-K (k_splits == kStreamK): CTA c takes the contiguous k-block range [c*U/G, (c+1)*U/G)
@@ -337,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
+  if (ep.ln_out != nullptr) ln_tail(ep, M, N);
 }
 
 // ---------------------------------------------------------------- CTA-pair variant
@@ -515,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc_cg2(tmem_base, Cfg::kTmemCols);
   }
+  if (ep.ln_out != nullptr) ln_tail(ep, M, N);
 }
 
 // Sum the K-split fp32 partials of 8 consecutive columns per thread and apply the fused epilogue
@@ -672,6 +800,10 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial,
                         int am) {
   if (M <= 0) return cudaSuccess;
+  if (ep.ln_out != nullptr &&
+      (ep.mode != kEpiAtomicF32 || ep.ln_bar == nullptr || ep.ln_x == nullptr || ep.ln_g == nullptr ||
+       ep.ln_b == nullptr || N % 8 != 0 || N / 8 > kThreads * kLnMaxVec || ep.ldc % 4 != 0))
+    return cudaErrorInvalidValue;
   if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
     if (k_splits == kStreamK && ep.mode != kEpiAtomicF32) return cudaErrorInvalidValue;
     if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;

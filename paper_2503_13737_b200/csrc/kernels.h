@@ -32,6 +32,17 @@ struct GemmEpilogue {
   int head_dim = 128;
   int block_size = 32;
   float* acc32 = nullptr;  // [M, ldc] fp32 (kEpiAtomicF32)
+  // Fused LayerNorm tail (kEpiAtomicF32 at TP=1; ln_out != null enables it): after a grid barrier
+  // (ln_bar: 2 words, zero-initialised, one per model/stream) every CTA finishes rows
+  // blockIdx.x, +gridDim.x, ...:  ln_x[r] = bf16(ln_x[r] + (acc32[r] + ln_bias));  acc32[r] = 0;
+  // ln_out[r] = LayerNorm(ln_x[r]) * ln_g + ln_b  -- what launch_layernorm_acc does as its own launch.
+  __nv_bfloat16* ln_x = nullptr;
+  const __nv_bfloat16* ln_bias = nullptr;
+  const __nv_bfloat16* ln_g = nullptr;
+  const __nv_bfloat16* ln_b = nullptr;
+  float ln_eps = 1e-5f;
+  __nv_bfloat16* ln_out = nullptr;
+  unsigned int* ln_bar = nullptr;
 };
 
 int make_tmap_kmajor(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld_elems,

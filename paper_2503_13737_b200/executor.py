@@ -157,6 +157,11 @@ class CudaExecutor:
         if getattr(self, "handle", None):
             self.lib.ag_model_destroy(self.handle)
             self.handle = None
+        # the KV pool (sized from free HBM by the bench / CLI) and the weights go back to torch's
+        # allocator even if a reference cycle keeps this object alive
+        self.kv = self.w = self.logits_buf = None
+        if getattr(self, "_swapped", None):
+            self._swapped.clear()
 
     def __del__(self):  # pragma: no cover
         try:

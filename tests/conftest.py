@@ -26,3 +26,23 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """GPU tests build OPT-13B/175B-shaped models, oracle executors on the device and KV pools sized
+    from free HBM; hand everything back to the driver between tests so a later test (the TP tests
+    spawn one process per rank on the same GPU) sees the whole 180 GB."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import gc
+    import torch
+    gc.collect()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        free, total = torch.cuda.mem_get_info()
+        if free < 0.6 * total:  # something outlived its test: name it in the log
+            print(f"\n[conftest] after {request.node.nodeid}: {free / 2**30:.1f} of {total / 2**30:.1f} GiB free",
+                  file=sys.stderr)

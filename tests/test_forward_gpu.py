@@ -170,13 +170,17 @@ def test_long_context_100k_vs_oracle_and_chunk_invariance():
     assert ta[0] == tb[0] and tda[0] == tdb[0]
 
 
-@pytest.mark.parametrize("bn,splits,am", [(128, 2, 128), (128, 5, 128), (128, 99, 128), (256, 99, 256),
-                                          (256, 2, 256)])  # 99 = stream-K (kStreamK); am 256 = CTA pair
-def test_split_k_atomic_epilogue_forward(bn, splits, am):
-    """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32 and the
-    next LayerNorm finishes bias + residual (and re-zeroes acc32); QKV / FC1 take the split-K reduce
+@pytest.mark.parametrize("bn,splits,am,fuse", [(128, 2, 128, "1"), (128, 5, 128, "1"), (128, 99, 128, "1"),
+                                               (256, 99, 256, "1"), (256, 2, 256, "1"), (128, 99, 128, "0"),
+                                               (256, 2, 256, "0")])  # 99 = stream-K (kStreamK); am 256 = CTA pair
+def test_split_k_atomic_epilogue_forward(bn, splits, am, fuse, monkeypatch):
+    """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32; the
+    residual + bias + next LayerNorm (which re-zeroes acc32) runs in the GEMM's own tail after a grid
+    barrier (AG_FUSE_LN, default) or as a separate LayerNorm launch (AG_FUSE_LN=0); the last FC2 is
+    always finished by the final LayerNorm on the logit rows.  QKV / FC1 take the split-K reduce
     kernel, or with stream-K (99) the atomic accumulator + finish kernel (q scale, KV scatter, ReLU).  Forced on for every M bucket via
     the plan table; two consecutive mixed steps vs the oracle (acc32 must be clean between steps)."""
+    monkeypatch.setenv("AG_FUSE_LN", fuse)
     import ctypes as C
     from paper_2503_13737_b200.executor import CudaExecutor
     from paper_2503_13737_b200.kvc import BlockPool
@@ -202,7 +206,7 @@ def test_split_k_atomic_epilogue_forward(bn, splits, am):
         b = _make_batch(pool, cfg, segs)
         a, r, r64 = dev.execute(b), ref.execute(b), ref64.execute(b)
         tally.add(a.logits, a.token_ids, r.logits, r.token_ids, r64.logits)
-    tally.check(f"plan {bn_}x{splits}a{am_}")
+    tally.check(f"plan {bn_}x{splits}a{am_} fuse_ln={fuse}")
 
 
 def test_175b_shape_two_layers_vs_oracle():

@@ -873,7 +873,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         if (out_atomic) {
           eo.mode = ag::kEpiAtomicF32;
           eo.acc32 = m->acc32;
-          if (m->fuse_ln) fuse_ln(eo, w.out_b, w.ln2_g, w.ln2_b);
+          if (m->fuse_ln && S <= ag::gemm_grid(S, H, m->hq, po.bn, po.k_splits, po.am))
+            fuse_ln(eo, w.out_b, w.ln2_g, w.ln2_b);
         } else if (!tp) {
           eo.bias = static_cast<const bf16*>(w.out_b);
           eo.residual = m->resid;
@@ -929,7 +930,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e2.ldc = H;
         ag::GemmPlan p2;
         const bool fc2_atomic = atomic_plan(L.tm_fc2, H, m->ffn_l, kGemmFc2, p2);
-        const bool fuse_next = fc2_atomic && m->fuse_ln && l + 1 < c.num_layers;
+        const bool fuse_next = fc2_atomic && m->fuse_ln && l + 1 < c.num_layers &&
+                               S <= ag::gemm_grid(S, H, m->ffn_l, p2.bn, p2.k_splits, p2.am);
         if (fc2_atomic) {
           e2.mode = ag::kEpiAtomicF32;
           e2.acc32 = m->acc32;
@@ -1167,7 +1169,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
           ed.ldr = H;
           ed.out = m->resid;
         }
-        const bool fused = with_ln && ed.mode == ag::kEpiAtomicF32 && m->fuse_ln;
+        const bool fused = with_ln && ed.mode == ag::kEpiAtomicF32 && m->fuse_ln &&
+                           M <= ag::gemm_grid(M, sh.N, sh.K, p.bn, p.k_splits, p.am);
         if (fused) {  // the forward's fused LayerNorm tail (one launch)
           ed.ln_x = m->resid;
           ed.ln_bias = bias_k;

@@ -190,7 +190,8 @@ AG_DEVICE uint4 bf16x8_pack(const float (&f)[8]) {
 }
 
 // Rows blockIdx.x, +gridDim.x, ... of  x = bf16(x + (acc + bias)); acc = 0; out = LN(x) * g + b  -- the
-// same rounding points as layernorm_row_kernel<float> (elementwise.cu), 256 threads per row.
+// same rounding points as layernorm_row_kernel<float> (elementwise.cu), 256 threads per row (a row per
+// warp instead was slower in-chain: 22.1 vs 20.8 ms on the median decode step -- too few loads in flight).
 AG_DEVICE void ln_tail(const GemmEpilogue& ep, int M, int hidden) {
   __shared__ float red[kThreads / 32];
   grid_barrier(ep.ln_bar, gridDim.x);
@@ -829,6 +830,14 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
   if (bn == 160) return launch_bn<160>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   if (bn == 64) return launch_bn<64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   return launch_bn<128>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
+}
+
+int gemm_grid(int M, int N, int K, int bn, int k_splits, int am) {
+  const int bm = am == 256 ? 256 : kBM;
+  const int64_t tiles = static_cast<int64_t>((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+  const int64_t units = k_splits == kStreamK ? tiles * ((K + kBK - 1) / kBK) : tiles * k_splits;
+  if (am == 256) return static_cast<int>(std::min<int64_t>(num_sms() & ~1, 2 * units));
+  return static_cast<int>(std::min<int64_t>(num_sms(), units));
 }
 
 cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& ep, cudaStream_t stream) {

@@ -65,6 +65,8 @@ struct GemmPlan {
   int am = 128;
 };
 GemmPlan plan_gemm(int M, int N, int K, int64_t partial_capacity_floats);
+// CTAs launch_gemm starts for this plan (max_ctas = 0)
+int gemm_grid(int M, int N, int K, int bn, int k_splits, int am);
 // Apply `ep` to a stream-K fp32 accumulator acc[M, N] (atomically filled) and re-zero it.
 cudaError_t launch_splitk_finish(float* acc, int M, int N, const GemmEpilogue& ep, cudaStream_t stream);
 

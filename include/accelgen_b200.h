@@ -231,6 +231,14 @@ AG_API int32_t ag_kv_swap_out(const void* pool, const int32_t* block_ids_dev, in
                        void* staging, void* stream);
 AG_API int32_t ag_kv_swap_in(const void* staging, const int32_t* block_ids_dev, int32_t n_blocks, int64_t block_elems,
                       void* pool, void* stream);
+/* The same over `planes` planes in one launch (every layer's K and V of a [L, 2, blocks, ...] pool):
+ * plane p of the pool starts at p * pool_plane_elems, of the staging buffer at p * stage_plane_elems. */
+AG_API int32_t ag_kv_swap_out_planes(const void* pool, int64_t pool_plane_elems, const int32_t* block_ids_dev,
+                              int32_t n_blocks, int64_t block_elems, void* staging, int64_t stage_plane_elems,
+                              int32_t planes, void* stream);
+AG_API int32_t ag_kv_swap_in_planes(const void* staging, int64_t stage_plane_elems, const int32_t* block_ids_dev,
+                             int32_t n_blocks, int64_t block_elems, void* pool, int64_t pool_plane_elems,
+                             int32_t planes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -91,6 +91,8 @@ _SIGS = {
     "ag_argmax": (i32, [vp, i32, i32, i32, i32, vp, vp, vp]),
     "ag_kv_swap_out": (i32, [vp, vp, i32, i64, vp, vp]),
     "ag_kv_swap_in": (i32, [vp, vp, i32, i64, vp, vp]),
+    "ag_kv_swap_out_planes": (i32, [vp, i64, vp, i32, i64, vp, i64, i32, vp]),
+    "ag_kv_swap_in_planes": (i32, [vp, i64, vp, i32, i64, vp, i64, i32, vp]),
 }
 
 _lock = threading.Lock()

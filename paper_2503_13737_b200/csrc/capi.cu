@@ -1536,4 +1536,26 @@ int32_t ag_kv_swap_in(const void* staging, const int32_t* block_ids_dev, int32_t
   return AG_OK;
 }
 
+int32_t ag_kv_swap_out_planes(const void* pool, int64_t pool_plane_elems, const int32_t* block_ids_dev,
+                              int32_t n_blocks, int64_t block_elems, void* staging, int64_t stage_plane_elems,
+                              int32_t planes, void* stream) {
+  if (!pool || !block_ids_dev || !staging) return fail(AG_EINVAL, "null pointer");
+  if (planes < 1 || n_blocks < 0) return fail(AG_EINVAL, "planes >= 1, n_blocks >= 0");
+  AG_CUDA(ag::launch_block_copy(static_cast<const bf16*>(pool), static_cast<bf16*>(staging), block_ids_dev, n_blocks,
+                                block_elems, true, static_cast<cudaStream_t>(stream), planes, pool_plane_elems,
+                                stage_plane_elems));
+  return AG_OK;
+}
+
+int32_t ag_kv_swap_in_planes(const void* staging, int64_t stage_plane_elems, const int32_t* block_ids_dev,
+                             int32_t n_blocks, int64_t block_elems, void* pool, int64_t pool_plane_elems,
+                             int32_t planes, void* stream) {
+  if (!pool || !block_ids_dev || !staging) return fail(AG_EINVAL, "null pointer");
+  if (planes < 1 || n_blocks < 0) return fail(AG_EINVAL, "planes >= 1, n_blocks >= 0");
+  AG_CUDA(ag::launch_block_copy(static_cast<const bf16*>(staging), static_cast<bf16*>(pool), block_ids_dev, n_blocks,
+                                block_elems, false, static_cast<cudaStream_t>(stream), planes, pool_plane_elems,
+                                stage_plane_elems));
+  return AG_OK;
+}
+
 }  // extern "C"

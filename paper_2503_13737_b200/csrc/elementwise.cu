@@ -422,19 +422,24 @@ __global__ void argmax_merge_kernel(const float* __restrict__ vals, const int32_
   out_idx[r] = i;
 }
 
+// Whole-block gather (swap out: pool -> staging) or scatter (swap in) over `planes` planes (layer x K/V):
+// plane p of the pool starts at p * pool_plane elements, of the staging buffer at p * stage_plane.
 __global__ void block_copy_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                   const int32_t* __restrict__ block_ids, int n_blocks, int64_t block_elems,
-                                  int gather) {
+                                  int gather, int planes, int64_t pool_plane, int64_t stage_plane) {
   pdl_trigger();
   pdl_wait();
   const int64_t vec_per_block = block_elems / 8;
-  const int64_t total = vec_per_block * n_blocks;
+  const int64_t per_plane = vec_per_block * n_blocks;
+  const int64_t total = per_plane * planes;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int b = static_cast<int>(i / vec_per_block);
-    const int64_t v = i - b * vec_per_block;
-    const int64_t pool_off = static_cast<int64_t>(block_ids[b]) * block_elems + v * 8;
-    const int64_t stage_off = static_cast<int64_t>(b) * block_elems + v * 8;
+    const int p = static_cast<int>(i / per_plane);
+    const int64_t j = i - p * per_plane;
+    const int b = static_cast<int>(j / vec_per_block);
+    const int64_t v = j - b * vec_per_block;
+    const int64_t pool_off = p * pool_plane + static_cast<int64_t>(block_ids[b]) * block_elems + v * 8;
+    const int64_t stage_off = p * stage_plane + static_cast<int64_t>(b) * block_elems + v * 8;
     if (gather)
       *reinterpret_cast<uint4*>(dst + stage_off) = *reinterpret_cast<const uint4*>(src + pool_off);
     else
@@ -584,12 +589,13 @@ cudaError_t launch_argmax_merge(const float* vals, const int32_t* idx, int tp, i
 }
 
 cudaError_t launch_block_copy(const __nv_bfloat16* src, __nv_bfloat16* dst, const int32_t* block_ids,
-                              int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream) {
-  if (n_blocks <= 0) return cudaSuccess;
-  if (block_elems % 8 != 0) return cudaErrorInvalidValue;
-  const int64_t work = block_elems / 8 * n_blocks;
+                              int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream, int planes,
+                              int64_t pool_plane, int64_t stage_plane) {
+  if (n_blocks <= 0 || planes <= 0) return cudaSuccess;
+  if (block_elems % 8 != 0 || pool_plane % 8 != 0 || stage_plane % 8 != 0) return cudaErrorInvalidValue;
+  const int64_t work = block_elems / 8 * n_blocks * planes;
   (void)launch_k(kPdlOther, block_copy_kernel, grid_for(work, 256), 256, 0, stream, src, dst, block_ids, n_blocks, block_elems,
-                                                             gather ? 1 : 0);
+                 gather ? 1 : 0, planes, pool_plane, stage_plane);
   return cudaGetLastError();
 }
 

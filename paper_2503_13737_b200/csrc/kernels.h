@@ -163,9 +163,12 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, int ld_src, const int32
                                int cols, __nv_bfloat16* dst, int ld_dst, cudaStream_t stream);
 
 // KV block swap: gather=true copies pool[block_ids[i]] -> dst[i] (contiguous staging);
-// gather=false copies src[i] -> dst[block_ids[i]] (staging back into the pool).
+// gather=false copies src[i] -> dst[block_ids[i]] (staging back into the pool).  planes > 1 repeats it
+// for plane p at element offsets p * pool_plane (pool) and p * stage_plane (staging): every layer's K and
+// V in one launch.
 cudaError_t launch_block_copy(const __nv_bfloat16* src, __nv_bfloat16* dst, const int32_t* block_ids,
-                              int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream);
+                              int n_blocks, int64_t block_elems, bool gather, cudaStream_t stream, int planes = 1,
+                              int64_t pool_plane = 0, int64_t stage_plane = 0);
 
 // pseudo-random bf16 fill (autotune activations): scale * U[-1, 1), optionally ReLU'd
 cudaError_t launch_fill_hash(__nv_bfloat16* x, int64_t n, uint32_t seed, float scale, bool relu,

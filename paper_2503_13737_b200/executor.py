@@ -263,6 +263,9 @@ class CudaExecutor:
         self._stage = [torch.empty(self.cfg.num_layers, 2, self._stage_blocks, self.heads_l, self.block_size,
                                    HEAD_DIM, dtype=torch.bfloat16, device=self.device)
                        for _ in range(self._SWAP_SLOTS)]
+        planes = self.cfg.num_layers * 2  # [L, 2, blocks, ...] viewed as [L*2, blocks, ...]
+        self._kv_planes = self.kv.view(planes, *self.kv.shape[2:])
+        self._stage_planes = [s.view(planes, *s.shape[2:]) for s in self._stage]
         self._slot_free = [None] * self._SWAP_SLOTS  # event after which the slot may be overwritten
         self._slot_keep = [[] for _ in range(self._SWAP_SLOTS)]  # host tensors the slot's copies still read
         self._next_slot = 0
@@ -340,9 +343,8 @@ class CudaExecutor:
             keep = self._slot_keep[slot]
             ids = self._ids_on_device(block_ids[c0:c0 + self._stage_blocks], keep)
             n = ids.numel()
-            for l in range(self.cfg.num_layers):
-                for kv in range(2):
-                    K.kv_swap_out(self.kv[l, kv], ids, stage[l, kv, :n])
+            # every layer's K and V in one launch (80 per-plane launches cost ~2 ms of host time per slot)
+            K.kv_swap_out_planes(self._kv_planes, ids, self._stage_planes[slot], n)
             gathered = torch.cuda.Event()
             gathered.record(comp)
             flat, host = self._host_chunk(n)
@@ -382,9 +384,7 @@ class CudaExecutor:
                 loaded.record(self._copy_stream)
             self._host_free.append((flat, loaded))  # reusable once its H2D copy is done
             comp.wait_event(loaded)
-            for l in range(self.cfg.num_layers):
-                for kv in range(2):
-                    K.kv_swap_in(stage[l, kv, :n], ids, self.kv[l, kv])
+            K.kv_swap_in_planes(self._stage_planes[slot], ids, self._kv_planes, n)
             scattered = torch.cuda.Event()
             scattered.record(comp)
             self._slot_free[slot] = scattered

@@ -150,6 +150,29 @@ def kv_swap_out(pool: torch.Tensor, block_ids: torch.Tensor, staging: torch.Tens
                                           staging.data_ptr(), _stream()))
 
 
+def kv_swap_out_planes(pool: torch.Tensor, block_ids: torch.Tensor, staging: torch.Tensor, n: int) -> None:
+    """staging[p, i] = pool[p, block_ids[i]] for every plane p (pool [P, blocks, ...], staging [P, slots, ...],
+    both contiguous; i < n): all layers' K and V of a preempted request in one launch."""
+    _need_cuda(pool, block_ids, staging)
+    if not (pool.is_contiguous() and staging.is_contiguous()) or pool.shape[0] != staging.shape[0]:
+        raise ValueError("kv_swap_out_planes: contiguous [planes, blocks, ...] pool and staging with equal planes")
+    block_elems = pool[0, 0].numel()
+    _lib.check(_lib.load().ag_kv_swap_out_planes(pool.data_ptr(), pool[0].numel(), block_ids.data_ptr(), n,
+                                                 block_elems, staging.data_ptr(), staging[0].numel(),
+                                                 pool.shape[0], _stream()))
+
+
+def kv_swap_in_planes(staging: torch.Tensor, block_ids: torch.Tensor, pool: torch.Tensor, n: int) -> None:
+    """pool[p, block_ids[i]] = staging[p, i] for every plane p and i < n."""
+    _need_cuda(pool, block_ids, staging)
+    if not (pool.is_contiguous() and staging.is_contiguous()) or pool.shape[0] != staging.shape[0]:
+        raise ValueError("kv_swap_in_planes: contiguous [planes, blocks, ...] pool and staging with equal planes")
+    block_elems = pool[0, 0].numel()
+    _lib.check(_lib.load().ag_kv_swap_in_planes(staging.data_ptr(), staging[0].numel(), block_ids.data_ptr(), n,
+                                                block_elems, pool.data_ptr(), pool[0].numel(), pool.shape[0],
+                                                _stream()))
+
+
 def kv_swap_in(staging: torch.Tensor, block_ids: torch.Tensor, pool: torch.Tensor) -> None:
     """pool[block_ids[i]] = staging[i]."""
     _need_cuda(pool, block_ids, staging)

@@ -255,3 +255,17 @@ def test_kv_swap_roundtrip(K):
     new_ids = torch.tensor([40, 41, 42, 43], dtype=torch.int32, device=DEV)
     K.kv_swap_in(staging, new_ids, pool)
     assert torch.equal(pool[new_ids.long()], pool[ids.long()])
+
+
+def test_kv_swap_planes_roundtrip(K):
+    """All layers' K and V planes of a [P, blocks, ...] pool in one launch, into the first n slots of a
+    larger staging ring slot and back into other blocks (byte-exact)."""
+    pool = _bf((6, 50, 2, 32, 128), 17).to(DEV)
+    ids = torch.tensor([4, 9, 0, 31, 7], dtype=torch.int32, device=DEV)
+    staging = torch.zeros(6, 8, 2, 32, 128, dtype=torch.bfloat16, device=DEV)
+    K.kv_swap_out_planes(pool, ids, staging, 5)
+    assert torch.equal(staging[:, :5], pool[:, ids.long()])
+    assert not staging[:, 5:].any()
+    new_ids = torch.tensor([40, 41, 42, 43, 44], dtype=torch.int32, device=DEV)
+    K.kv_swap_in_planes(staging, new_ids, pool, 5)
+    assert torch.equal(pool[:, new_ids.long()], pool[:, ids.long()])

@@ -221,9 +221,9 @@ struct ag_model {
   float* acc_big = nullptr;  // fp32 [T, max(3*hq, ffn)] stream-K accumulator of QKV / FC1 (zero between uses)
   int64_t acc_big_cols = 0;
   bool deterministic = false;  // AG_DETERMINISTIC=1: no fp32 atomics (split-K via the reduce kernel)
-  // TP=1 atomic out-proj / FC2 finish residual + bias + the next LayerNorm in their own tail (grid
-  // barrier on ln_bar) instead of a launch_layernorm_acc launch; AG_FUSE_LN=0 turns it off
-  bool fuse_ln = true;
+  // AG_FUSE_LN=1: the LayerNorm finishing a TP=1 atomic out-proj / FC2 runs in the consuming QKV / FC1
+  // GEMM's prologue (or the atomic GEMM's tail) behind a grid barrier instead of its own launch
+  bool fuse_ln = false;
   unsigned int* ln_bar = nullptr;
   int64_t splitk_cap = 0;
   GemmTable tune;
@@ -353,7 +353,7 @@ cudaError_t gemm_w(const ActMap& a, const WeightMap& w, int M, int N, int K, con
 cudaError_t gemm_planned(const ActMap& a, const WeightMap& w, int M, int N, int K, const ag::GemmEpilogue& ep,
                          const ag::GemmPlan& p, cudaStream_t s, float* splitk_ws, int64_t splitk_cap, float* acc_big) {
   if (p.k_splits != ag::kStreamK) return gemm_w(a, w, M, N, K, ep, s, splitk_ws, splitk_cap, nullptr, -1, &p);
-  ag::GemmEpilogue ea;
+  ag::GemmEpilogue ea = ep;  // keeps a fused LayerNorm prologue (the finish kernel ignores it)
   ea.mode = ag::kEpiAtomicF32;
   ea.acc32 = acc_big;
   ea.ldc = N;
@@ -529,8 +529,11 @@ int32_t ag_model_create(const ag_model_config* cfg, ag_model** out) {
   {
     const char* e = std::getenv("AG_DETERMINISTIC");
     m->deterministic = e && e[0] == '1';
+    // off by default: in-chain it gains <= 0.1 ms per decode step without the cooperative attribute, and
+    // the cooperative launch its grid barrier needs (profiler replay failed without it) costs +0.45 ms
+    // (profiles/r2/fused_ln/README.md)
     const char* f = std::getenv("AG_FUSE_LN");
-    m->fuse_ln = !(f && f[0] == '0');
+    m->fuse_ln = f && f[0] == '1';
   }
   chk(dmalloc(&m->ln_bar, 64));
   if (r == AG_OK && cudaMemset(m->ln_bar, 0, 64 * sizeof(unsigned int)) != cudaSuccess) r = fail(AG_ECUDA, "memset ln_bar");
@@ -789,6 +792,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
     bool ln1_done = false;  // the previous FC2's fused tail already wrote this layer's LN1 (xln)
     // fused LayerNorm tail on an atomic out-proj / FC2 (see ag::GemmEpilogue::ln_out)
     auto fuse_ln = [&](ag::GemmEpilogue& e, const void* bias, const void* g, const void* b) {
+      e.ln_acc = m->acc32;
+      e.ln_ld = H;
       e.ln_x = m->resid;
       e.ln_bias = static_cast<const bf16*>(bias);
       e.ln_g = static_cast<const bf16*>(g);
@@ -797,10 +802,20 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
       e.ln_out = m->xln;
       e.ln_bar = m->ln_bar;
     };
+    // QKV / FC1 plans (the same for every layer at this S): a consumer whose grid covers the S rows
+    // finishes the previous atomic out-proj / FC2's LayerNorm in its prologue (preferred: its weight
+    // prefetch overlaps the norm); otherwise the atomic GEMM's own tail does when its grid covers them
+    ag::GemmPlan pq = pick_plan(m->layers[0].tm_qkv, S, 3 * m->hq, H, m->splitk_cap, &m->tune, kGemmQkv);
+    if (m->deterministic && pq.k_splits == ag::kStreamK) pq.k_splits = 1;
+    ag::GemmPlan p1 = pick_plan(m->layers[0].tm_fc1, S, m->ffn_l, H, m->splitk_cap, &m->tune, kGemmFc1);
+    if (m->deterministic && p1.k_splits == ag::kStreamK) p1.k_splits = 1;
+    const bool qkv_prologue = m->fuse_ln && !tp && S <= ag::gemm_grid(S, 3 * m->hq, H, pq.bn, pq.k_splits, pq.am);
+    const bool fc1_prologue = m->fuse_ln && !tp && S <= ag::gemm_grid(S, m->ffn_l, H, p1.bn, p1.k_splits, p1.am);
     for (int l = 0; l < c.num_layers; ++l) {
       const LayerState& L = m->layers[l];
       const ag_layer_weights& w = L.w;
-      if (!ln1_done) {
+      const bool ln1_in_qkv = acc_pending && qkv_prologue;
+      if (!ln1_done && !ln1_in_qkv) {
         // LN1 (for TP the previous layer's FC2 all-reduce result + bias is folded in here)
         ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, ((tp || acc_pending) && l > 0) ? 2.0 * ln_bytes : ln_bytes);
         if (acc_pending) {  // previous layer's FC2 was split-K into acc32: finish its epilogue here
@@ -832,9 +847,13 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         ep.heads = m->heads_l;
         ep.head_dim = m->head_dim;
         ep.block_size = c.block_size;
-        ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H), gemm_bytes(S, 3 * m->hq, H, 2));
-        ag::GemmPlan pq = pick_plan(L.tm_qkv, S, 3 * m->hq, H, m->splitk_cap, &m->tune, kGemmQkv);
-        if (m->deterministic && pq.k_splits == ag::kStreamK) pq.k_splits = 1;
+        if (ln1_in_qkv) {  // the previous FC2's reductions + LN1, in this GEMM's prologue
+          fuse_ln(ep, m->layers[l - 1].w.fc2_b, w.ln1_g, w.ln1_b);
+          ep.ln_prologue = 1;
+          acc_pending = false;
+        }
+        ProfScope ps(m, AG_K_QKV_GEMM, s, gemm_flops(S, 3 * m->hq, H),
+                     gemm_bytes(S, 3 * m->hq, H, 2) + (ln1_in_qkv ? 2.0 * ln_bytes : 0.0));
         AG_CUDA(gemm_planned(m->tm_xln, L.tm_qkv, S, 3 * m->hq, H, ep, pq, s, m->splitk_ws, m->splitk_cap, m->acc_big));
         AG_TRY(dbg(s, "qkv_gemm", l));
       }
@@ -873,7 +892,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         if (out_atomic) {
           eo.mode = ag::kEpiAtomicF32;
           eo.acc32 = m->acc32;
-          if (m->fuse_ln && S <= ag::gemm_grid(S, H, m->hq, po.bn, po.k_splits, po.am))
+          if (m->fuse_ln && !fc1_prologue && S <= ag::gemm_grid(S, H, m->hq, po.bn, po.k_splits, po.am))
             fuse_ln(eo, w.out_b, w.ln2_g, w.ln2_b);
         } else if (!tp) {
           eo.bias = static_cast<const bf16*>(w.out_b);
@@ -900,6 +919,8 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         AG_CUDA(ag::launch_layernorm(m->resid, m->proj, static_cast<const bf16*>(w.out_b), nullptr,
                                      static_cast<const bf16*>(w.ln2_g), static_cast<const bf16*>(w.ln2_b), c.ln_eps, S,
                                      H, m->xln, s));
+      } else if (acc_pending && fc1_prologue) {
+        // LN2 runs in FC1's prologue (below)
       } else if (acc_pending) {
         ProfScope ps(m, AG_K_LAYERNORM, s, 0.0, 2.0 * ln_bytes);
         AG_CUDA(ag::launch_layernorm_acc(m->resid, m->acc32, static_cast<const bf16*>(w.out_b), nullptr,
@@ -919,9 +940,14 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e1.relu = 1;
         e1.out = m->ffn;
         e1.ldc = m->ffn_l;
-        ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H), gemm_bytes(S, m->ffn_l, H, 2));
-        ag::GemmPlan p1 = pick_plan(L.tm_fc1, S, m->ffn_l, H, m->splitk_cap, &m->tune, kGemmFc1);
-        if (m->deterministic && p1.k_splits == ag::kStreamK) p1.k_splits = 1;
+        const bool ln2_in_fc1 = acc_pending && fc1_prologue;
+        if (ln2_in_fc1) {  // the out-proj's reductions + LN2, in this GEMM's prologue
+          fuse_ln(e1, w.out_b, w.ln2_g, w.ln2_b);
+          e1.ln_prologue = 1;
+          acc_pending = false;
+        }
+        ProfScope ps(m, AG_K_FC1_GEMM, s, gemm_flops(S, m->ffn_l, H),
+                     gemm_bytes(S, m->ffn_l, H, 2) + (ln2_in_fc1 ? 2.0 * ln_bytes : 0.0));
         AG_CUDA(gemm_planned(m->tm_xln, L.tm_fc1, S, m->ffn_l, H, e1, p1, s, m->splitk_ws, m->splitk_cap, m->acc_big));
         AG_TRY(dbg(s, "fc1_gemm", l));
       }
@@ -930,7 +956,7 @@ int32_t ag_model_forward_staged(ag_model* m, int32_t* out_tokens_dev, float* log
         e2.ldc = H;
         ag::GemmPlan p2;
         const bool fc2_atomic = atomic_plan(L.tm_fc2, H, m->ffn_l, kGemmFc2, p2);
-        const bool fuse_next = fc2_atomic && m->fuse_ln && l + 1 < c.num_layers &&
+        const bool fuse_next = fc2_atomic && m->fuse_ln && !qkv_prologue && l + 1 < c.num_layers &&
                                S <= ag::gemm_grid(S, H, m->ffn_l, p2.bn, p2.k_splits, p2.am);
         if (fc2_atomic) {
           e2.mode = ag::kEpiAtomicF32;
@@ -1172,6 +1198,8 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         const bool fused = with_ln && ed.mode == ag::kEpiAtomicF32 && m->fuse_ln &&
                            M <= ag::gemm_grid(M, sh.N, sh.K, p.bn, p.k_splits, p.am);
         if (fused) {  // the forward's fused LayerNorm tail (one launch)
+          ed.ln_acc = m->acc32;
+          ed.ln_ld = H;
           ed.ln_x = m->resid;
           ed.ln_bias = bias_k;
           ed.ln_g = static_cast<const bf16*>(w0.ln2_g);

@@ -320,21 +320,38 @@ inline int ablate_mask() {
   return mask;
 }
 
+// coop: cooperative launch -- the runtime guarantees every CTA is co-resident (or fails the launch), which a
+// kernel with a grid-wide barrier (the GEMMs' fused LayerNorm) needs under MPS / profiler replay too.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                     Args&&... args) {
+cudaError_t launch_k_ex(int cls, bool coop, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t stream, Args&&... args) {
   if (ablate_mask() & cls) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled(cls)) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  return launch_k_ex(cls, false, kernel, grid, block, smem, stream, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------- misc

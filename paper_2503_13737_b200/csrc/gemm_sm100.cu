@@ -192,13 +192,12 @@ AG_DEVICE uint4 bf16x8_pack(const float (&f)[8]) {
 // Rows blockIdx.x, +gridDim.x, ... of  x = bf16(x + (acc + bias)); acc = 0; out = LN(x) * g + b  -- the
 // same rounding points as layernorm_row_kernel<float> (elementwise.cu), 256 threads per row (a row per
 // warp instead was slower in-chain: 22.1 vs 20.8 ms on the median decode step -- too few loads in flight).
-AG_DEVICE void ln_tail(const GemmEpilogue& ep, int M, int hidden) {
+AG_DEVICE void ln_rows(const GemmEpilogue& ep, int M, int hidden) {
   __shared__ float red[kThreads / 32];
-  grid_barrier(ep.ln_bar, gridDim.x);
   const int nvec = hidden / 8;
   for (int r = blockIdx.x; r < M; r += gridDim.x) {
     __nv_bfloat16* xr = ep.ln_x + static_cast<int64_t>(r) * hidden;
-    float4* ar = reinterpret_cast<float4*>(ep.acc32 + static_cast<int64_t>(r) * ep.ldc);
+    float4* ar = reinterpret_cast<float4*>(ep.ln_acc + static_cast<int64_t>(r) * ep.ln_ld);
     float v[kLnMaxVec][8];
     float sum = 0.0f;
 #pragma unroll
@@ -250,6 +249,19 @@ AG_DEVICE void ln_tail(const GemmEpilogue& ep, int M, int hidden) {
       }
     }
   }
+}
+
+// Fused LayerNorm prologue of the *consumer* GEMM (QKV after an atomic FC2, FC1 after an atomic
+// out-proj): the predecessor left its fp32 reductions in ln_acc; this grid's CTAs -- resident, their
+// first weight stages already in flight -- finish the rows into ln_out (= this GEMM's A operand), make the
+// generic stores visible to the TMA (async proxy) and meet at a grid barrier before any A tile is loaded.
+// Unlike the producer-side tail, the next GEMM's weight prefetch overlaps the norm.
+AG_DEVICE void ln_prologue(const GemmEpilogue& ep, int M, int K) {
+  pdl_wait();
+  ln_rows(ep, M, K);
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // writer side: generic stores -> async proxy
+  grid_barrier(ep.ln_bar, gridDim.x);
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // reader side: before this CTA's TMA loads of A
 }
 
 // Work decomposition shared by the three warp roles of the 1-CTA kernel.  Classic: unit t =
@@ -343,27 +355,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
+  // weights of a small-M GEMM are streamed once -> evict first (large M reuses a weight tile across
+  // concurrent m-blocks)
+  const uint64_t pol_w = num_m <= 2 ? policy_evict_first() : policy_evict_normal();
+  // The weight k-blocks of the first S stages do not depend on the predecessor kernel: the producer
+  // issues them before griddepcontrol.wait (and before a fused LayerNorm prologue), so the weight
+  // stream starts while the predecessor drains.
+  int pre = 0;
+  if (warp == 0 && lane == 0) {
+    SegIter ip(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
+    while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
+      for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
+        mbar_arrive_expect_tx(&full_bar[pre], Cfg::kStageBytes);
+        tma_load_2d_hint(sB + pre * Cfg::kBBytes, &tmap_b, &full_bar[pre], kb * kBK, n_blk * BN, pol_w);
+      }
+  }
+  if (ep.ln_out != nullptr && ep.ln_prologue) ln_prologue(ep, M, K);
+
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      // activations are re-read by every N tile -> keep in L2; weights of a small-M GEMM are
-      // streamed once -> evict first (large M reuses a weight tile across concurrent m-blocks)
+      // activations are re-read by every N tile -> keep in L2
       const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_w = num_m <= 2 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(M, N, K, kBM, BN, k_splits, blockIdx.x, gridDim.x);
-      // The weight k-blocks of the first S stages do not depend on the predecessor kernel: issue
-      // them before griddepcontrol.wait, so the weight stream starts while the predecessor drains.
-      int pre = 0;
-      {
-        SegIter ip = it;
-        while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
-          for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
-            mbar_arrive_expect_tx(&full_bar[pre], Cfg::kStageBytes);
-            tma_load_2d_hint(sB + pre * Cfg::kBBytes, &tmap_b, &full_bar[pre], kb * kBK, n_blk * BN, pol_w);
-          }
-      }
       pdl_wait();
       int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
@@ -464,7 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
-  if (ep.ln_out != nullptr) ln_tail(ep, M, N);
+  if (ep.ln_out != nullptr && !ep.ln_prologue) {  // fused tail: every CTA's reductions have drained
+    grid_barrier(ep.ln_bar, gridDim.x);
+    ln_rows(ep, M, N);
+  }
 }
 
 // ---------------------------------------------------------------- CTA-pair variant
@@ -529,25 +548,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   pdl_trigger();  // after the TMEM allocation (see the 1-CTA kernel)
   const uint32_t tmem_base = *tmem_slot;
 
+  const uint64_t pol_w = num_m <= 1 ? policy_evict_first() : policy_evict_normal();
+  const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);
+  int pre = 0;  // weight k-blocks issued before griddepcontrol.wait (see the 1-CTA kernel)
+  if (warp == 0 && lane == 0) {
+    SegIter ip(M, N, K, 256, BN, k_splits, pair, num_pairs);
+    while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
+      for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
+        if (rank == 0) mbar_arrive_expect_tx(&full_bar[pre], 2 * Cfg::kStageBytes);
+        tma_load_2d_cg2(sB + pre * Cfg::kBBytes, &tmap_b, full0 + pre * 8, kb * kBK, n_blk * BN + rank * (BN / 2),
+                        pol_w);
+      }
+  }
+  if (ep.ln_out != nullptr && ep.ln_prologue) ln_prologue(ep, M, K);
+
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs): own 128 A rows + own BN/2 B rows per k-block
       const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_w = num_m <= 1 ? policy_evict_first() : policy_evict_normal();
-      const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(M, N, K, 256, BN, k_splits, pair, num_pairs);
-      int pre = 0;  // weight k-blocks issued before griddepcontrol.wait (see the 1-CTA kernel)
-      {
-        SegIter ip = it;
-        while (pre < S && ip.next(m_blk, n_blk, ks, kb0, kb1))
-          for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
-            if (rank == 0) mbar_arrive_expect_tx(&full_bar[pre], 2 * Cfg::kStageBytes);
-            tma_load_2d_cg2(sB + pre * Cfg::kBBytes, &tmap_b, full0 + pre * 8, kb * kBK, n_blk * BN + rank * (BN / 2),
-                            pol_w);
-          }
-      }
       pdl_wait();
       int g = 0;
       while (it.next(m_blk, n_blk, ks, kb0, kb1)) {
@@ -643,7 +664,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc_cg2(tmem_base, Cfg::kTmemCols);
   }
-  if (ep.ln_out != nullptr) ln_tail(ep, M, N);
+  if (ep.ln_out != nullptr && !ep.ln_prologue) {  // fused tail: every CTA's reductions have drained
+    grid_barrier(ep.ln_bar, gridDim.x);
+    ln_rows(ep, M, N);
+  }
 }
 
 // Sum the K-split fp32 partials of 8 consecutive columns per thread and apply the fused epilogue
@@ -762,8 +786,10 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, int M
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (units < grid) grid = static_cast<int>(units);
-  (void)launch_k(kPdlGemm, gemm_bf16_tn_kernel<BN, AM>, grid, kThreads, Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
+  const cudaError_t le = launch_k_ex(kPdlGemm, ep.ln_out != nullptr, gemm_bf16_tn_kernel<BN, AM>, grid, kThreads,
+                                     Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = le;
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
@@ -788,8 +814,10 @@ static cudaError_t launch_bn2(const CUtensorMap& ta, const CUtensorMap& tb, int 
   int grid = num_sms() & ~1;
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas & ~1;
   if (2 * units < grid) grid = static_cast<int>(2 * units);
-  (void)launch_k(kPdlGemm, gemm2_bf16_tn_kernel<BN>, grid, kThreads, Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
+  const cudaError_t le = launch_k_ex(kPdlGemm, ep.ln_out != nullptr, gemm2_bf16_tn_kernel<BN>, grid, kThreads,
+                                     Cfg::kSmemBytes, stream, ta, tb, M, N, K, ep, k_splits, partial);
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = le;
   if (e != cudaSuccess || k_splits == 1 || ep.mode == kEpiAtomicF32) return e;
   const int64_t work = static_cast<int64_t>(M) * (N / 8);
   int rg = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
@@ -801,10 +829,13 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
                         const GemmEpilogue& ep, int max_ctas, cudaStream_t stream, int k_splits, float* partial,
                         int am) {
   if (M <= 0) return cudaSuccess;
-  if (ep.ln_out != nullptr &&
-      (ep.mode != kEpiAtomicF32 || ep.ln_bar == nullptr || ep.ln_x == nullptr || ep.ln_g == nullptr ||
-       ep.ln_b == nullptr || N % 8 != 0 || N / 8 > kThreads * kLnMaxVec || ep.ldc % 4 != 0))
-    return cudaErrorInvalidValue;
+  if (ep.ln_out != nullptr) {
+    const int hidden = ep.ln_prologue ? K : N;
+    if ((!ep.ln_prologue && ep.mode != kEpiAtomicF32) || ep.ln_bar == nullptr || ep.ln_x == nullptr ||
+        ep.ln_acc == nullptr || ep.ln_g == nullptr || ep.ln_b == nullptr || hidden % 8 != 0 ||
+        hidden / 8 > kThreads * kLnMaxVec || ep.ln_ld % 4 != 0)
+      return cudaErrorInvalidValue;
+  }
   if (am == 256) {  // CTA pair: ta box = 128 rows, tb box = bn/2 rows
     if (k_splits == kStreamK && ep.mode != kEpiAtomicF32) return cudaErrorInvalidValue;
     if (k_splits > 1 && ep.mode != kEpiAtomicF32 && (partial == nullptr || N % 32 != 0)) return cudaErrorInvalidValue;

@@ -32,10 +32,16 @@ struct GemmEpilogue {
   int head_dim = 128;
   int block_size = 32;
   float* acc32 = nullptr;  // [M, ldc] fp32 (kEpiAtomicF32)
-  // Fused LayerNorm tail (kEpiAtomicF32 at TP=1; ln_out != null enables it): after a grid barrier
-  // (ln_bar: 2 words, zero-initialised, one per model/stream) every CTA finishes rows
-  // blockIdx.x, +gridDim.x, ...:  ln_x[r] = bf16(ln_x[r] + (acc32[r] + ln_bias));  acc32[r] = 0;
-  // ln_out[r] = LayerNorm(ln_x[r]) * ln_g + ln_b  -- what launch_layernorm_acc does as its own launch.
+  // Fused LayerNorm (TP=1; ln_out != null enables it; ln_bar: 2 words, zero-initialised, one per
+  // model/stream).  Every CTA finishes rows blockIdx.x, +gridDim.x, ... of
+  //   ln_x[r] = bf16(ln_x[r] + (ln_acc[r] + ln_bias));  ln_acc[r] = 0;  ln_out[r] = LN(ln_x[r]) * ln_g + ln_b
+  // -- what launch_layernorm_acc does as its own launch.  Tail (ln_prologue = 0; kEpiAtomicF32 with
+  // ln_acc = acc32): after this GEMM's reductions, behind a grid barrier.  Prologue (ln_prologue = 1):
+  // before this GEMM loads any A tile (ln_out is its A operand; ln_acc holds the predecessor's
+  // reductions), while its first weight stages are in flight.
+  int ln_prologue = 0;
+  float* ln_acc = nullptr;
+  int ln_ld = 0;
   __nv_bfloat16* ln_x = nullptr;
   const __nv_bfloat16* ln_bias = nullptr;
   const __nv_bfloat16* ln_g = nullptr;

@@ -55,6 +55,9 @@ class CudaExecutor:
         # never-written slots hold finite values
         self.kv = torch.zeros(cfg.num_layers, 2, num_blocks, heads_l, self.block_size, HEAD_DIM,
                               dtype=torch.bfloat16, device=self.device)
+        # weight init's fp32 temporaries stay in torch's cache; the library's own cudaMallocs (activations,
+        # workspaces) need that HBM back -- with several ranks sharing one GPU (host TP backend) they failed
+        torch.cuda.empty_cache()
 
         mc = _lib.ModelConfig(hidden=cfg.hidden, num_layers=cfg.num_layers, num_heads=cfg.num_heads, ffn=cfg.ffn,
                               vocab=cfg.vocab, pos_rows=cfg.pos_rows, tp_rank=tp_rank, tp_size=tp_size,

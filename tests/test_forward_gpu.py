@@ -175,8 +175,9 @@ def test_long_context_100k_vs_oracle_and_chunk_invariance():
                                                (256, 2, 256, "0")])  # 99 = stream-K (kStreamK); am 256 = CTA pair
 def test_split_k_atomic_epilogue_forward(bn, splits, am, fuse, monkeypatch):
     """Out-proj / FC2 split-K at TP=1 accumulate fp32 partials with red.global.add into acc32; the
-    residual + bias + next LayerNorm (which re-zeroes acc32) runs in the GEMM's own tail after a grid
-    barrier (AG_FUSE_LN, default) or as a separate LayerNorm launch (AG_FUSE_LN=0); the last FC2 is
+    residual + bias + next LayerNorm (which re-zeroes acc32) runs, when the step has no more rows than
+    the consuming QKV / FC1 GEMM has CTAs, in that GEMM's prologue behind a grid barrier (else in the
+    atomic GEMM's tail, else as its own launch; AG_FUSE_LN=0: always its own launch); the last FC2 is
     always finished by the final LayerNorm on the logit rows.  QKV / FC1 take the split-K reduce
     kernel, or with stream-K (99) the atomic accumulator + finish kernel (q scale, KV scatter, ReLU).  Forced on for every M bucket via
     the plan table; two consecutive mixed steps vs the oracle (acc32 must be clean between steps)."""
@@ -202,7 +203,10 @@ def test_split_k_atomic_epilogue_forward(bn, splits, am, fuse, monkeypatch):
     ref = OracleExecutor(cfg, w, pool.total_blocks, device="cuda")
     ref64 = OracleExecutor(cfg, w, pool.total_blocks, device="cuda", acc=torch.float64)
     tally = Tally()
-    for segs in ([(0, 0, 700), (1, 0, 60)], [(0, 700, 1), (1, 60, 200), (2, 0, 33)]):
+    # the third step (3 decodes) has fewer rows than any plan's CTAs: the fused LayerNorm runs in the
+    # QKV / FC1 prologue (or the atomic GEMM's tail) instead of its own launch
+    for segs in ([(0, 0, 700), (1, 0, 60)], [(0, 700, 1), (1, 60, 200), (2, 0, 33)],
+                 [(0, 701, 1), (1, 260, 1), (2, 33, 1)]):
         b = _make_batch(pool, cfg, segs)
         a, r, r64 = dev.execute(b), ref.execute(b), ref64.execute(b)
         tally.add(a.logits, a.token_ids, r.logits, r.token_ids, r64.logits)

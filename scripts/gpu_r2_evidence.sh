@@ -13,12 +13,12 @@ echo "launch list rc=$?" >> gpurun_out/${TAG}_log.txt
 python scripts/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_summary.txt 2>&1
 timeout 1500 ncu --profile-from-start off --set full --clock-control none --import-source on \
   -k regex:"mixed_attention|gemm" --launch-count ${NFULL:-12} -o gpurun_out/${TAG}_bench_full \
-  env AG_NCU_TIMED=1 python bench.py --steps 1 --warmup 1 --ramp-s $RAMP --no-cpu-baseline \
+  env AG_NCU_TIMED=1 python bench.py --steps 1 --warmup 1 --ramp-s $RAMP --no-cpu-baseline --kv-gb ${NCU_KV_GB:-40} \
   > gpurun_out/${TAG}_full.out 2> gpurun_out/${TAG}_full.err
 echo "full rc=$?" >> gpurun_out/${TAG}_log.txt
 python scripts/ncu_summary.py gpurun_out/${TAG}_bench_full.ncu-rep > gpurun_out/${TAG}_full_summary.txt 2>&1
 if [ -z "$SKIP_TP" ]; then
-timeout 900 python bench.py --gpus 2 --tp-backend host --steps 3 --warmup 1 --ramp-s 20 --rate 1 \
+timeout 900 python bench.py --gpus 2 --tp-backend host --steps 3 --warmup 1 --ramp-s 20 --rate 1 --kv-gb 20 \
   > gpurun_out/${TAG}_tp2.out 2> gpurun_out/${TAG}_tp2.err
 echo "tp2 rc=$?" >> gpurun_out/${TAG}_log.txt
 fi

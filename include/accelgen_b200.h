@@ -195,8 +195,7 @@ AG_API int64_t ag_model_last_h2d_bytes(ag_model* m);
 /* ---- individual kernels (device pointers), for parity tests and the profiler ---- */
 /* D[M,N] = A[M,K] . W[N,K]^T (+bias[N]) (+residual[M,ldr]) (ReLU); bf16 out unless out_f32.
  * block_n in {0 (auto), 64, 128, 256}; k_splits 0 = auto (uses workspace, fp32 k_splits*M*N);
- * a_rows in {0/128, 96, 64, 32}: activation rows staged per k-block (small-M variant needs M <= a_rows);
- * 256 = CTA pair. */
+ * a_rows in {0/128, 64, 32}: activation rows staged per k-block (small-M variant needs M <= a_rows). */
 AG_API int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, const void* bias,
                      const void* residual, int32_t ldr, int32_t relu, void* D, int32_t ldd, int32_t out_f32,
                      int32_t M, int32_t N, int32_t K, int32_t block_n, int32_t k_splits, int32_t a_rows,

@@ -175,10 +175,8 @@ struct WeightMap {
 
 // Activation operand maps for the three A-box heights (128 rows; 32/64 for small-M GEMMs).
 struct ActMap {
-  CUtensorMap box32, box64, box96, box128;
-  const CUtensorMap& box(int am) const {
-    return am == 32 ? box32 : (am == 64 ? box64 : (am == 96 ? box96 : box128));
-  }
+  CUtensorMap box32, box64, box128;
+  const CUtensorMap& box(int am) const { return am == 32 ? box32 : (am == 64 ? box64 : box128); }
 };
 
 // Autotuned (BLOCK_N, k_splits, A rows) per GEMM kind and M bucket (ag_model_autotune).
@@ -367,7 +365,6 @@ cudaError_t gemm_planned(const ActMap& a, const WeightMap& w, int M, int N, int 
 int32_t amap(ActMap* a, const void* ptr, int64_t rows, int64_t k, const char* what) {
   AG_TRY(tmap(&a->box32, ptr, rows, k, 32, what));
   AG_TRY(tmap(&a->box64, ptr, rows, k, 64, what));
-  AG_TRY(tmap(&a->box96, ptr, rows, k, 96, what));
   return tmap(&a->box128, ptr, rows, k, 128, what);
 }
 
@@ -1098,7 +1095,7 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
   const int H = c.hidden;
   GemmTable& t = m->tune;
   t.m_bucket.clear();
-  for (int mb : {16, 32, 64, 96, 128, 192, 256, 320, 384, 448, 512, 640, 768, 896, 1024, 1280, 1536, 2048, 3072, 4096,
+  for (int mb : {16, 32, 64, 128, 192, 256, 320, 384, 448, 512, 640, 768, 896, 1024, 1280, 1536, 2048, 3072, 4096,
                  6144, 8192, 12288, 16384})
     if (mb < c.max_tokens) t.m_bucket.push_back(mb);
   t.m_bucket.push_back(c.max_tokens);
@@ -1133,21 +1130,19 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
     shapes[kGemmFc2].w.push_back(&L.tm_fc2);
   }
   std::vector<ag::GemmPlan> cands;
-  for (int am : {256, 128, 96, 64, 32})
+  for (int am : {256, 128, 64, 32})
     for (const ag::GemmPlan& q : {ag::GemmPlan{256, 1}, ag::GemmPlan{128, 1}, ag::GemmPlan{64, 1},
                                   ag::GemmPlan{256, 2}, ag::GemmPlan{128, 2}, ag::GemmPlan{64, 2},
                                   ag::GemmPlan{256, 3}, ag::GemmPlan{256, 4}, ag::GemmPlan{128, 4},
                                   ag::GemmPlan{64, 4}, ag::GemmPlan{256, 6}, ag::GemmPlan{128, 6},
                                   ag::GemmPlan{256, 8}, ag::GemmPlan{128, 8}})
       cands.push_back({q.bn, q.k_splits, am});
-  for (int am : {128, 96, 64, 32})  // stream-K (atomic fp32 epilogue; finished by LayerNorm or the finish kernel)
+  for (int am : {128, 64, 32})  // stream-K (atomic fp32 epilogue; finished by LayerNorm or the finish kernel)
     for (int bn : {256, 128, 64}) cands.push_back({bn, ag::kStreamK, am});
-  for (int am : {128, 96, 64, 32})
+  for (int am : {128, 64, 32})
     for (int ks : {1, 2}) cands.push_back({160, ks, am});
   cands.push_back({256, ag::kStreamK, 256});  // stream-K over CTA pairs
   cands.push_back({128, ag::kStreamK, 256});
-  const char* na = std::getenv("AG_TUNE_NO_AM96");  // A/B switch: without the 96-row A stages
-  const bool no_am96 = na && na[0] == '1';
   cudaEvent_t e0, e1;
   AG_CUDA(cudaEventCreate(&e0));
   AG_CUDA(cudaEventCreate(&e1));
@@ -1176,7 +1171,6 @@ int32_t ag_model_autotune(ag_model* m, void* stream) {
         if (p.bn == 256 && !sh.w[0]->has256 && p.am != 256) continue;
         if (p.bn == 160 && (!sh.w[0]->has160 || p.am == 256)) continue;
         if (p.am < 128 && M > p.am) continue;
-        if (p.am == 96 && no_am96) continue;
         if (p.k_splits == ag::kStreamK) {
           if (k == kGemmLm || (p.am == 256 && M <= 128)) continue;
           if ((k == kGemmOut || k == kGemmFc2) && c.tp_size != 1) continue;
@@ -1277,7 +1271,7 @@ int32_t ag_model_set_gemm_plans(ag_model* m, const int32_t* rows, int32_t n) {
     const int kind = rows[4 * i], mb = rows[4 * i + 1], bn = rows[4 * i + 2], ks = rows[4 * i + 3] % 100,
               am = rows[4 * i + 3] / 100;
     if (kind < 0 || kind >= kGemmKinds || mb <= 0 || (bn != 64 && bn != 128 && bn != 160 && bn != 256) || ks < 1 ||
-        (am != 32 && am != 64 && am != 96 && am != 128 && am != 256))
+        (am != 32 && am != 64 && am != 128 && am != 256))
       return fail(AG_EINVAL, "bad gemm plan row " + std::to_string(i));
     if (kind == 0) t.m_bucket.push_back(mb);
     t.plan[kind].push_back(ag::GemmPlan{bn, ks, am});
@@ -1402,8 +1396,8 @@ int32_t ag_gemm_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, con
                      int32_t block_n, int32_t k_splits, int32_t a_rows, void* workspace, int64_t workspace_bytes,
                      void* stream) {
   if (a_rows == 0) a_rows = 128;
-  if (a_rows != 32 && a_rows != 64 && a_rows != 96 && a_rows != 128 && a_rows != 256)
-    return fail(AG_EINVAL, "a_rows must be 32, 64, 96, 128 or 256 (CTA pair)");
+  if (a_rows != 32 && a_rows != 64 && a_rows != 128 && a_rows != 256)
+    return fail(AG_EINVAL, "a_rows must be 32, 64, 128 or 256 (CTA pair)");
   if (a_rows < 128 && M > a_rows) return fail(AG_EINVAL, "a_rows < M");
   if (a_rows == 256 && block_n != 128 && block_n != 256) return fail(AG_EINVAL, "CTA pair needs block_n 128/256");
   if (!A || !W || !D) return fail(AG_EINVAL, "null pointer");

@@ -851,12 +851,6 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     if (bn == 64) return launch_bn<64, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     return launch_bn<128, 32>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
   }
-  if (am == 96) {  // 65..96 rows: 12 KB A stages, one more weight stage in flight than AM = 128
-    if (bn == 256) return launch_bn<256, 96>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
-    if (bn == 160) return launch_bn<160, 96>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
-    if (bn == 64) return launch_bn<64, 96>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
-    return launch_bn<128, 96>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
-  }
   if (am == 64) {
     if (bn == 256) return launch_bn<256, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);
     if (bn == 160) return launch_bn<160, 64>(ta, tb, M, N, K, ep, k_splits, partial, max_ctas, stream);

@@ -44,9 +44,7 @@ def test_gemm_matches_fp32(K, M, N, K_, bn, splits):
 
 @pytest.mark.parametrize("M,N,K_,bn,splits,a_rows", [(1, 5120, 5120, 128, 1, 32), (32, 15360, 5120, 256, 2, 32),
                                                      (40, 20480, 5120, 160, 1, 64), (17, 3200, 2048, 160, 2, 32),
-                                                     (60, 2048, 20480, 64, 4, 64), (64, 20480, 5120, 256, 1, 64),
-                                                     (96, 15360, 5120, 128, 1, 96), (65, 5120, 20480, 160, 2, 96),
-                                                     (90, 20480, 5120, 160, 1, 96)])
+                                                     (60, 2048, 20480, 64, 4, 64), (64, 20480, 5120, 256, 1, 64)])
 def test_gemm_small_m_variant(K, M, N, K_, bn, splits, a_rows):
     """Small-M path: only `a_rows` activation rows are staged; stale rows feed masked outputs only."""
     a, w = _bf((M, K_), 21), _bf((N, K_), 22, 0.05)

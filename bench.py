@@ -207,7 +207,11 @@ def run_ours(args):
                       init="opt", nccl_uid=uid, host_collective=host_coll)
     # preemption swaps: staging ring in HBM + host chunks pinned now rather than on the serving path
     import psutil
-    ex.prepare_swap(min(48.0, 0.3 * psutil.virtual_memory().available / 1e9 / max(1, world)))
+    # (a fresh 0.5 GB pinned chunk on the serving path costs ~0.1 s of host time; r2end ran out of a
+    # 48 GB pool at 4 req/s)
+    host_avail_gb = psutil.virtual_memory().available / 1e9
+    pinned_pool_gb = min(96.0, 0.4 * host_avail_gb / max(1, world))
+    ex.prepare_swap(pinned_pool_gb)
     torch.cuda.synchronize()
     free_after_setup = torch.cuda.mem_get_info()[0]
 
@@ -279,6 +283,7 @@ def run_ours(args):
     ex.set_profiling(False)  # the timed windows run un-instrumented; kernel classes come from a replay
     launches0, h2d0, d2h0 = ex.launches, ex.h2d_bytes, ex.d2h_bytes
     plan0, swap0 = eng.plan_host_s, getattr(ex, "swap_host_s", 0.0)
+    sec0 = dict(getattr(ex, "swap_section_s", {}))
     sampler = ClockSampler(local % n_dev)
     sampler.start()
     torch.cuda.synchronize()
@@ -440,7 +445,11 @@ def run_ours(args):
         "swap_gb_total": getattr(ex, "swap_bytes", 0) / 1e9,
         "swap_host": {"blocked_s_total": getattr(ex, "swap_wait_s", 0.0), "blocked_waits": getattr(ex, "swap_waits", 0),
                       "pageable": bool(getattr(ex, "_pin_failed", False)),
-                      "host_chunks": getattr(ex, "swap_host_chunks", 0)},
+                      "host_chunks": getattr(ex, "swap_host_chunks", 0),
+                      "pinned_pool_gb": round(pinned_pool_gb, 1), "host_avail_gb_at_setup": round(host_avail_gb, 1),
+                      # host seconds per swap-path section inside the timed windows
+                      "section_s": {k: round(v - sec0.get(k, 0.0), 3)
+                                    for k, v in getattr(ex, "swap_section_s", {}).items()}},
         "hbm_gb": {"kv_pool": num_blocks * 32 * kv_tok_bytes / 1e9, "free_after_setup": free_after_setup / 1e9,
                    "free_at_end": torch.cuda.mem_get_info()[0] / 1e9},
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,

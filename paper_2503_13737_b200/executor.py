@@ -278,6 +278,7 @@ class CudaExecutor:
         self.swap_bytes = 0
         self.swap_wait_s, self.swap_waits = 0.0, 0  # host time blocked on a draining staging slot
         self.swap_host_s = 0.0  # host time inside swap_out / swap_in (launches, pinned allocation, waits)
+        self.swap_section_s = {"acquire_slot": 0.0, "host_chunk": 0.0, "ids": 0.0, "enqueue": 0.0}
 
     def _acquire_slot(self) -> int:
         i = self._next_slot
@@ -340,23 +341,34 @@ class CudaExecutor:
         t_host = time.perf_counter()
         comp = torch.cuda.current_stream(self.device)
         host_chunks = []
+        sec = self.swap_section_s
         for c0 in range(0, len(block_ids), self._stage_blocks):
+            t = time.perf_counter()
             slot = self._acquire_slot()
+            sec["acquire_slot"] += time.perf_counter() - t
             stage = self._stage[slot]
             keep = self._slot_keep[slot]
+            t = time.perf_counter()
             ids = self._ids_on_device(block_ids[c0:c0 + self._stage_blocks], keep)
+            sec["ids"] += time.perf_counter() - t
             n = ids.numel()
+            t = time.perf_counter()
             # every layer's K and V in one launch (80 per-plane launches cost ~2 ms of host time per slot)
             K.kv_swap_out_planes(self._kv_planes, ids, self._stage_planes[slot], n)
             gathered = torch.cuda.Event()
             gathered.record(comp)
+            sec["enqueue"] += time.perf_counter() - t
+            t = time.perf_counter()
             flat, host = self._host_chunk(n)
+            sec["host_chunk"] += time.perf_counter() - t
+            t = time.perf_counter()
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(gathered)
                 host.copy_(stage[:, :, :n], non_blocking=host.is_pinned())
                 done = torch.cuda.Event()
                 done.record(self._copy_stream)
             self._slot_free[slot] = done
+            sec["enqueue"] += time.perf_counter() - t
             host_chunks.append((flat, host))
             self.swap_bytes += host.numel() * 2
         self._swapped[request_id] = host_chunks
@@ -375,12 +387,18 @@ class CudaExecutor:
         t_host = time.perf_counter()
         comp = torch.cuda.current_stream(self.device)
         at = 0
+        sec = self.swap_section_s
         for flat, host in host_chunks:
             n = host.shape[2]
+            t = time.perf_counter()
             slot = self._acquire_slot()
+            sec["acquire_slot"] += time.perf_counter() - t
             stage = self._stage[slot]
             keep = self._slot_keep[slot]
+            t = time.perf_counter()
             ids = self._ids_on_device(block_ids[at:at + n], keep)
+            sec["ids"] += time.perf_counter() - t
+            t = time.perf_counter()
             with torch.cuda.stream(self._copy_stream):  # same stream as the swap-out D2H: ordered after it
                 stage[:, :, :n].copy_(host, non_blocking=host.is_pinned())
                 loaded = torch.cuda.Event()
@@ -391,6 +409,7 @@ class CudaExecutor:
             scattered = torch.cuda.Event()
             scattered.record(comp)
             self._slot_free[slot] = scattered
+            sec["enqueue"] += time.perf_counter() - t
             self.swap_bytes += host.numel() * 2
             at += n
         self.swap_host_s += time.perf_counter() - t_host

@@ -315,6 +315,7 @@ def run_ours(args):
     if orig_submit is not None:
         ex.submit = orig_submit
     plan_s, swap_s = eng.plan_host_s - plan0, getattr(ex, "swap_host_s", 0.0) - swap0
+    sec_win = {k: v - sec0.get(k, 0.0) for k, v in getattr(ex, "swap_section_s", {}).items()}
     recs = [it for w in windows for it in w]
     if not recs:
         raise SystemExit(f"no forward completed in the {args.steps} timed windows (engine clock {eng.clock:.1f} s, "
@@ -448,8 +449,7 @@ def run_ours(args):
                       "host_chunks": getattr(ex, "swap_host_chunks", 0),
                       "pinned_pool_gb": round(pinned_pool_gb, 1), "host_avail_gb_at_setup": round(host_avail_gb, 1),
                       # host seconds per swap-path section inside the timed windows
-                      "section_s": {k: round(v - sec0.get(k, 0.0), 3)
-                                    for k, v in getattr(ex, "swap_section_s", {}).items()}},
+                      "section_s": {k: round(v, 3) for k, v in sec_win.items()}},
         "hbm_gb": {"kv_pool": num_blocks * 32 * kv_tok_bytes / 1e9, "free_after_setup": free_after_setup / 1e9,
                    "free_at_end": torch.cuda.mem_get_info()[0] / 1e9},
         "decode_tokens_per_step": sum(r.num_decode for r in recs) / K,

@@ -210,7 +210,9 @@ def run_ours(args):
     # (a fresh 0.5 GB pinned chunk on the serving path costs ~0.1 s of host time; r2end ran out of a
     # 48 GB pool at 4 req/s)
     host_avail_gb = psutil.virtual_memory().available / 1e9
-    pinned_pool_gb = min(128.0, 0.5 * host_avail_gb / max(1, world))
+    # (half of the available RAM, 105 GB, stopped pinning at ~78 GB on the B200 box: the rest of the
+    # chunks fell back to pageable memory and synchronous copies, profiles/r2/rate_sweep.md)
+    pinned_pool_gb = min(96.0, 0.4 * host_avail_gb / max(1, world))
     ex.prepare_swap(pinned_pool_gb)
     torch.cuda.synchronize()
     free_after_setup = torch.cuda.mem_get_info()[0]

@@ -312,6 +312,12 @@ class CudaExecutor:
             if ready is None or ready.query():
                 del self._host_free[i]
                 return flat, flat[: n * per_block].view(shape)
+        flat = self._alloc_chunk()
+        return flat, flat[: n * per_block].view(shape)
+
+    def _alloc_chunk(self) -> torch.Tensor:
+        """A fresh slot-sized host chunk: pinned, or pageable once the OS refuses to lock more pages."""
+        per_block = self._stage[0][:, :, 0].numel()
         flat = None
         if not getattr(self, "_pin_failed", False):
             try:
@@ -321,16 +327,20 @@ class CudaExecutor:
         if flat is None:
             flat = torch.empty(self._stage_blocks * per_block, dtype=torch.bfloat16)
         self.swap_host_chunks += 1
-        return flat, flat[: n * per_block].view(shape)
+        return flat
 
     def prepare_swap(self, host_gb: float) -> None:
         """Allocate the staging ring and pin ~host_gb of host chunks up front (bench setup), so the first
         preemptions do not page-lock memory on the serving path."""
         self._swap_init()
         n = int(host_gb * 1e9 // (self._stage_blocks * self._stage[0][:, :, 0].numel() * 2))
+        # fresh chunks only: _host_chunk would hand back the chunk just added (the pool stayed at one
+        # chunk and every preemption page-locked memory on the serving path)
         for _ in range(max(0, n)):
-            flat, _ = self._host_chunk(1)
-            self._host_free.append((flat, None))
+            chunk = self._alloc_chunk()
+            if getattr(self, "_pin_failed", False):  # the OS refused: a pageable pool would only add sync copies
+                break
+            self._host_free.append((chunk, None))
 
     def swap_out(self, request_id: int, block_ids: list[int], tokens: int) -> None:
         """Preemption (reference BlockPool.preempt, kvc.py:153-160): the request's KV blocks of every

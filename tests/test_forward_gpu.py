@@ -234,8 +234,8 @@ def test_175b_shape_two_layers_vs_oracle():
     tally.check("175B-shape 2 layers")
 
 
-@pytest.mark.parametrize("per_chunk", [3, 1])
-def test_executor_swap_roundtrip_chunked(per_chunk):
+@pytest.mark.parametrize("per_chunk,pool", [(3, 0), (1, 0), (1, 5)])
+def test_executor_swap_roundtrip_chunked(per_chunk, pool):
     """Preemption swap through the executor (kvc.py:153-160 preempt / demand_readmit): a request's
     blocks of every layer go to host memory through the HBM staging ring in several chunks (1 block per
     chunk: 8 chunks cycle the 4-slot ring twice) without host synchronisation, the freed blocks are
@@ -246,6 +246,10 @@ def test_executor_swap_roundtrip_chunked(per_chunk):
     w = M.init_weights(cfg, seed=0, init="test")
     dev = CudaExecutor(cfg, 64, max_tokens=256, max_seqs=8, weights=w, autotune=False)
     dev._SWAP_STAGE_BYTES = per_chunk * cfg.num_layers * 2 * dev.heads_l * 32 * 128 * 2
+    if pool:  # host chunks pinned up front (bench setup): `pool` distinct buffers, reused by the swaps
+        dev.prepare_swap(pool * dev._SWAP_STAGE_BYTES / 1e9)
+        ptrs = {flat.data_ptr() for flat, _ in dev._host_free}
+        assert len(ptrs) == len(dev._host_free) == pool and dev.swap_host_chunks == pool
     g = torch.Generator(device="cuda").manual_seed(3)
     dev.kv.copy_(torch.randn(dev.kv.shape, generator=g, device="cuda").to(torch.bfloat16))
     src = [5, 9, 2, 40, 41, 17, 63, 0]
